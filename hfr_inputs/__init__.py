@@ -1,0 +1,95 @@
+"""Seeded synthetic input generators shared by tests, smoke() and bench.py.
+
+This module holds NONE of the method's arithmetic: it only draws random
+per-rank gradient buffers (numpy) with the shapes and value distributions
+DESIGN.md §"Input recipe" lists. Both the oracle (oracle/) and the CUDA path
+(paper_2408_14158_b200/) consume these arrays; neither side imports the other.
+
+Dtype encoding: fp32 buffers are ``np.float32`` arrays; bf16 buffers are
+``np.uint16`` arrays holding the raw bfloat16 bit patterns.  bf16 values are
+obtained by TRUNCATING a float32 draw to its top 16 bits (round-toward-zero
+bit slicing), which is input generation, not the method's RNE cast.
+
+Seeds follow SURVEY.md §8d: ``np.random.default_rng(base + rank)``.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+FP32 = "f32"
+BF16 = "bf16"
+
+# Distribution names:
+#   normal     N(0, 1)
+#   grad       N(0, 1e-3^2)  gradient-like (C2)
+#   int        integers, |x| < 2^20 for fp32 (every partial sum exact for n <= 8),
+#              |x| <= 256 for bf16 (bf16-exact, fp32 sums exact in any order)
+#   loguniform magnitudes log-uniform in [2^-20, 2^4], random sign (C3)
+#   specials   mixture of +-0, subnormals, +-Inf, NaN, 2^24 and 1 (C1 (iii))
+DISTS = ("normal", "grad", "int", "loguniform", "specials")
+
+
+def _draw_f32(rng: np.random.Generator, dist: str, count: int, dtype: str) -> np.ndarray:
+    if dist == "normal":
+        return rng.standard_normal(count, dtype=np.float32)
+    if dist == "grad":
+        return (rng.standard_normal(count, dtype=np.float32) * np.float32(1e-3)).astype(np.float32)
+    if dist == "int":
+        lim = (1 << 20) - 1 if dtype == FP32 else 256
+        return rng.integers(-lim, lim + 1, size=count, dtype=np.int64).astype(np.float32)
+    if dist == "loguniform":
+        e = rng.uniform(-20.0, 4.0, size=count)
+        s = rng.choice(np.array([-1.0, 1.0]), size=count)
+        return (s * np.exp2(e)).astype(np.float32)
+    if dist == "specials":
+        pool = np.array(
+            [0.0, -0.0, 1.0, -1.0, 2.0 ** 24, 1.5, np.inf, -np.inf, np.nan,
+             np.float32(1e-40), np.float32(-1e-40), np.float32(1.17549435e-38),
+             np.float32(3.4e38), np.float32(-3.4e38), np.float32(2.0 ** -149)],
+            dtype=np.float32)
+        pick = rng.integers(0, len(pool), size=count)
+        out = pool[pick]
+        # a third of the entries are ordinary normals so the mix is not all-special
+        mask = rng.random(count) < 0.33
+        out[mask] = rng.standard_normal(int(mask.sum()), dtype=np.float32)
+        return out
+    raise ValueError(f"unknown distribution {dist!r}")
+
+
+def _to_dtype(x: np.ndarray, dtype: str) -> np.ndarray:
+    if dtype == FP32:
+        return np.ascontiguousarray(x, dtype=np.float32)
+    if dtype == BF16:
+        return (np.ascontiguousarray(x, dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    raise ValueError(f"unknown dtype {dtype!r}")
+
+
+def rank_input(rank: int, count: int, dtype: str = FP32, dist: str = "normal",
+               seed_base: int = 1234) -> np.ndarray:
+    """One rank's buffer: ``count`` elements drawn with ``default_rng(seed_base + rank)``."""
+    rng = np.random.default_rng(seed_base + rank)
+    return _to_dtype(_draw_f32(rng, dist, count, dtype), dtype)
+
+
+def rank_inputs(nranks: int, count: int, dtype: str = FP32, dist: str = "normal",
+                seed_base: int = 1234) -> list[np.ndarray]:
+    """Buffers for all ranks of one allreduce (list index = communicator rank)."""
+    return [rank_input(r, count, dtype, dist, seed_base) for r in range(nranks)]
+
+
+def low_bits_cleared(x: np.ndarray, bits: int) -> np.ndarray:
+    """fp32 array with the low ``bits`` mantissa bits zeroed (for the n*x invariant)."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    return (u & np.uint32((0xFFFFFFFF << bits) & 0xFFFFFFFF)).view(np.float32)
+
+
+# Paper-scale sizes.
+C1_COUNT = 4096                      # config 1: 2 ranks x 4096 fp32
+C2_COUNT = 186 * (1 << 20) // 4      # config 2: 186 MiB fp32 = 48,758,784 elements
+C5_BUCKET_BYTES = 64 << 20           # config 5: 64 MiB buckets
+C5_PARAMS = 7_000_000_000            # config 5: 7B bf16 gradient volume
+
+
+def c3_sizes_bytes() -> list[int]:
+    """config 3: message sizes 1 KiB .. 1 GiB (powers of two)."""
+    return [1024 << k for k in range(21)]
