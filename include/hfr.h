@@ -1,0 +1,184 @@
+/* hfr.h — C ABI of the B200-native HFReduce library (libhfr.so).
+ *
+ * HFReduce is the hierarchical, asynchronous gradient allreduce of
+ * Fire-Flyer AI-HPC (arXiv 2408.14158), PAPER.md:296-398 (§4).  On one
+ * 8xB200 NVSwitch box the GPUs play the role of the paper's nodes and every
+ * transfer is an SM load/store over NVLink on CUDA-IPC-mapped memory; the
+ * reduction is an fp32 fold on the SMs.
+ *
+ * Conventions for every function below
+ *   - Returns an hfr_status_t; never aborts the process.
+ *   - Pointers named buf / ptr are DEVICE pointers on the comm's CUDA device;
+ *     all other pointers are host pointers.
+ *   - A `stream` is a cudaStream_t passed as an opaque pointer (no CUDA types
+ *     in this header).  0 is the legacy default stream.
+ *   - Thread-compatible: one comm per process per device; calls on one comm
+ *     must not race.
+ *   - Collective calls (marked COLLECTIVE) must be made by every rank of the
+ *     comm, in the same order, with matching arguments.
+ */
+#ifndef HFR_H_
+#define HFR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HFR_MAX_RANKS 16
+
+typedef struct hfr_comm_s* hfr_comm_t;
+typedef struct hfr_req_s* hfr_req_t;
+typedef void* hfr_stream_t; /* cudaStream_t */
+
+/* Element types.  bf16 is reduced with fp32 accumulation and ONE final RNE
+ * rounding (reading R2; PAPER.md:404 lists FP32/FP16/BF16/FP8). */
+typedef enum { HFR_FLOAT32 = 0, HFR_BFLOAT16 = 1 } hfr_dtype_t;
+
+/* Reduction operator.  The paper's only operator is the sum ("reduction add
+ * operation"). */
+typedef enum { HFR_SUM = 0 } hfr_op_t;
+
+typedef enum {
+    HFR_SUCCESS = 0,
+    HFR_ERR_INVALID_ARGUMENT = 1, /* NULL buf with count > 0, bad rank/nranks, unknown enum, bad config */
+    HFR_ERR_UNSUPPORTED = 2,      /* valid but not implemented (op != SUM, PAIR_DBT with odd n, ...) */
+    HFR_ERR_CUDA = 3,             /* a CUDA runtime call failed; see hfr_last_cuda_error() */
+    HFR_ERR_OUT_OF_MEMORY = 4,
+    HFR_ERR_PROTOCOL = 5,         /* ranks disagree on count/dtype/op/algo/buffer/call order */
+    HFR_ERR_TIMEOUT = 6,          /* a cross-rank spin wait exceeded timeout_ms */
+    HFR_ERR_NOT_INITIALIZED = 7,  /* NULL or finalized comm / request */
+    HFR_ERR_INTERNAL = 8
+} hfr_status_t;
+
+/* Allreduce schedules (the three subsystems of DESIGN.md §1).
+ *   FLAT     reduce-scatter + all-gather in one fused pass: rank g pulls shard g
+ *            of all n buffers over NVLink, folds in rank order 0..n-1 (fp32),
+ *            scales, casts, and stores the result into all n buffers.  Result =
+ *            rank-ascending fold (Algorithm 1 order).
+ *   DBT      the paper's double binary tree (Algorithm 2) as
+ *            a push-only P2P schedule over the GPUs; chunk c rides tree c mod 2.
+ *   PAIR_DBT "HFReduce with NVLink": pair (2k,2k+1) reduce,
+ *            tree over the n/2 pair partials per half, pair all-gather.
+ *   AUTO     = FLAT. */
+typedef enum { HFR_ALGO_AUTO = 0, HFR_ALGO_FLAT = 1, HFR_ALGO_DBT = 2, HFR_ALGO_PAIR_DBT = 3 } hfr_algo_t;
+
+/* All-gather callback used ONLY by the collective setup calls (hfr_init,
+ * hfr_mem_alloc, hfr_register, hfr_finalize) to exchange CUDA IPC handles:
+ * gather `bytes` from every rank into recv[nranks*bytes] in rank order.
+ * Returns 0 on success.  Typically a torch.distributed all_gather. */
+typedef int (*hfr_allgather_fn)(const void* send, void* recv, size_t bytes, void* ctx);
+
+typedef struct {
+    int algo;             /* hfr_algo_t */
+    size_t chunk_elems;   /* tree chunk size in elements (Alg. 1 "Chunk_Size");
+                             multiple of 256; 0 -> 8192.  Changes DBT/PAIR_DBT bits (reading R8),
+                             never FLAT's. */
+    int max_ctas;         /* CTAs per rank; 0 -> one per SM.  Caps the SMs the comm uses. */
+    int threads;          /* threads per CTA (128..512, multiple of 32); 0 -> 512 */
+    float scale;          /* gradient scale, multiplies the fp32 total once (reading R3); 1.0 = sum */
+    size_t scratch_bytes; /* per-rank library scratch (staging + tree partials); 0 -> 256 MiB */
+    int timeout_ms;       /* cross-rank spin-wait timeout; 0 -> 60000 */
+} hfr_config_t;
+
+/* Fill *cfg with the defaults above (algo AUTO, scale 1.0). */
+void hfr_config_default(hfr_config_t* cfg);
+
+/* COLLECTIVE.  Create a communicator for `rank` of `nranks` (1..HFR_MAX_RANKS)
+ * processes, each driving one GPU of this box (`cuda_device`).  Allocates the
+ * peer-mapped signal pad and scratch, exchanges CUDA IPC handles through
+ * `allgather(ctx)`, opens the peers' mappings.  cfg may be NULL (defaults).
+ * On success *comm is owned by the caller until hfr_finalize.
+ * Errors: INVALID_ARGUMENT (comm NULL, rank out of range, nranks out of range,
+ * allgather NULL with nranks > 1, bad cfg), CUDA, OUT_OF_MEMORY. */
+hfr_status_t hfr_init(hfr_comm_t* comm, int rank, int nranks, int cuda_device,
+                      hfr_allgather_fn allgather, void* ctx, const hfr_config_t* cfg);
+
+/* Single-process communicator with `nranks` VIRTUAL ranks on one GPU: every
+ * kernel launch runs all ranks' CTAs at once (cooperative launch), peer
+ * "NVLink" accesses become local HBM accesses.  Same kernels, same protocol;
+ * used for the 1-GPU bench line and the 1-GPU parity tests. */
+hfr_status_t hfr_init_virtual(hfr_comm_t* comm, int nranks, int cuda_device, const hfr_config_t* cfg);
+
+/* COLLECTIVE.  Change algo / scale / chunk_elems / max_ctas / threads for
+ * subsequent calls (scratch_bytes and timeout_ms are fixed at init). */
+hfr_status_t hfr_comm_set_config(hfr_comm_t comm, const hfr_config_t* cfg);
+
+/* Number of ranks this process drives: 1 for hfr_init comms, nranks for
+ * virtual comms.  Also rank / nranks queries. */
+int hfr_comm_local_ranks(hfr_comm_t comm);
+int hfr_comm_rank(hfr_comm_t comm);
+int hfr_comm_nranks(hfr_comm_t comm);
+
+/* COLLECTIVE.  Allocate `bytes` of symmetric peer-mapped device memory.
+ * ptrs receives hfr_comm_local_ranks(comm) pointers (one per local rank).
+ * Buffers inside such memory are reduced zero-copy (no staging).  Freed by
+ * hfr_mem_free (collective) or hfr_finalize. */
+hfr_status_t hfr_mem_alloc(hfr_comm_t comm, size_t bytes, void** ptrs);
+hfr_status_t hfr_mem_free(hfr_comm_t comm, void* ptr);
+
+/* COLLECTIVE.  Make an existing cudaMalloc'ed range [ptr, ptr+bytes) peer
+ * visible (its whole allocation is IPC-exported and opened by every peer).
+ * Idempotent per allocation.  Real comms only (virtual comms: no-op). */
+hfr_status_t hfr_register(hfr_comm_t comm, void* ptr, size_t bytes);
+
+/* COLLECTIVE, asynchronous.  In-place sum-allreduce of `count` elements of
+ * `dtype` at device pointer `buf` ("Dg: data need to allreduce",
+ * :367 "Dg_i is allreduced").
+ *   Ordering: starts after all work already enqueued on `stream`; returns to
+ *   the host immediately.  If req != NULL the work runs on the comm's side
+ *   stream and *req must be passed to hfr_wait exactly once; if req == NULL it
+ *   runs on `stream` itself (completion is stream-ordered).
+ *   Result: every rank's buf holds identical bytes: the rank-ascending fold
+ *   (FLAT), the tree-order fold (DBT) or the pair-first fold (PAIR_DBT), times
+ *   scale, cast to dtype.  Buffers outside hfr_mem_alloc / hfr_register memory
+ *   or not 16-byte aligned are staged through the scratch (correct, slower).
+ *   Ownership: caller owns buf; it must stay allocated and untouched until
+ *   completion.
+ *   Errors (returned now): NOT_INITIALIZED, INVALID_ARGUMENT (buf NULL with
+ *   count > 0, unknown dtype), UNSUPPORTED (op != SUM), CUDA.  count == 0 is a
+ *   successful no-op.  Cross-rank errors (PROTOCOL, TIMEOUT) surface at
+ *   hfr_wait / hfr_comm_status. */
+hfr_status_t hfr_allreduce(hfr_comm_t comm, void* buf, size_t count, hfr_dtype_t dtype,
+                           hfr_op_t op, hfr_stream_t stream, hfr_req_t* req);
+
+/* Virtual-comm form: bufs[r] is virtual rank r's buffer (all on the comm's
+ * device).  Same semantics as hfr_allreduce. */
+hfr_status_t hfr_allreduce_virtual(hfr_comm_t comm, void* const* bufs, size_t count, hfr_dtype_t dtype,
+                                   hfr_op_t op, hfr_stream_t stream, hfr_req_t* req);
+
+/* Complete a request.  stream != NULL: make `stream` wait for it (no host
+ * block; pass (hfr_stream_t)1 = cudaStreamLegacy for the legacy default
+ * stream).  stream == NULL: block the host until done and report PROTOCOL /
+ * TIMEOUT / CUDA errors raised by the kernels.  Releases req. */
+hfr_status_t hfr_wait(hfr_req_t req, hfr_stream_t stream);
+
+/* Non-blocking check: SUCCESS, or the sticky cross-rank error seen so far. */
+hfr_status_t hfr_comm_status(hfr_comm_t comm);
+
+/* COLLECTIVE.  Device-side barrier across all ranks, enqueued on `stream`
+ * (used to align ranks before a timed region). */
+hfr_status_t hfr_barrier(hfr_comm_t comm, hfr_stream_t stream);
+
+/* COLLECTIVE.  Synchronise, barrier, unmap peers, free everything. */
+hfr_status_t hfr_finalize(hfr_comm_t comm);
+
+/* Host-only query of the double binary tree the DBT schedule uses (reading
+ * R9): for tree `which` (0 = A, 1 = B) over n ranks, fills parent[n] (-1 at
+ * the root) and child0[n], child1[n] (children in ascending rank, -1 if
+ * absent).  No GPU needed. */
+hfr_status_t hfr_tree_query(int n, int which, int* parent, int* child0, int* child1);
+
+/* Kernel launches this comm has issued (for bench.py's gpu_launches). */
+uint64_t hfr_comm_launches(hfr_comm_t comm);
+
+const char* hfr_status_string(hfr_status_t s);
+/* Text of the last CUDA error seen by this thread's calls (or ""). */
+const char* hfr_last_cuda_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HFR_H_ */

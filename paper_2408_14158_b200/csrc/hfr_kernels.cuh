@@ -1,0 +1,532 @@
+// hfr_kernels.cuh — sm_100a kernels of the B200-native HFReduce.
+//
+// Paper: Fire-Flyer AI-HPC, arXiv 2408.14158, §4 HFReduce.
+// The paper's CPU-side steps (D2H copy, SIMD reduce-add, RDMA double binary
+// tree, H2D copy) become SM loads/stores over NVLink on CUDA-IPC-mapped
+// memory.  Every kernel takes an Args by value holding, per rank r, the
+// pointer (valid in this process) to rank r's buffer, tree partials and
+// signal pad.  In a virtual comm all ranks live on one GPU and one launch
+// runs every rank's CTAs (blockIdx.y = rank - rank0).
+//
+// Numerics (readings R1-R6): fp32 adds/multiplies via __fadd_rn /
+// __fmul_rn (never contracted into FMA, no FTZ since the TU is built without
+// --use_fast_math), bf16 widened exactly, fp32 accumulate, one RNE cast.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace hfr {
+
+constexpr int kMaxRanks = 16;
+constexpr int kMaxCtas = 1024;
+constexpr int kMaxChunks = 65536;
+
+// Peer-mapped signal pad, one per rank (DESIGN.md §5 "HBM layout").
+// entry/sig/exit[b][q] are written by rank q's CTA b; up/down/pdown[c] are the
+// per-chunk tree flags (c = chunk index local to the launch).  All values are
+// launch epochs, strictly increasing per comm, so nothing is ever reset.
+struct Pad {
+  uint64_t entry[kMaxCtas][kMaxRanks];
+  uint64_t sig[kMaxCtas][kMaxRanks];
+  uint64_t exit[kMaxCtas][kMaxRanks];
+  uint64_t up[2][kMaxChunks];   // child partial for chunk c landed in slot s
+  uint64_t down[kMaxChunks];    // final chunk c landed in my buffer (from tree parent)
+  uint64_t pdown[kMaxChunks];   // final chunk c of my other half landed (from pair partner)
+};
+
+// One node of a double binary tree (reading R9/R10).  Children are sorted by
+// rank; self_pos = number of children with a smaller rank, so the in-order
+// combination is  children[0..self_pos) , x_v , children[self_pos..nchild).
+struct TreeNode {
+  int8_t parent;    // -1 at the root
+  int8_t nchild;    // 0..2
+  int8_t self_pos;  // 0..nchild
+  int8_t slot;      // my slot index in my parent's sorted children
+  int8_t child[2];
+  int8_t pad_[2];
+};
+
+struct Args {
+  char* buf[kMaxRanks];    // rank r's data buffer (this call)
+  float* part[kMaxRanks];  // rank r's fp32 partial slots (tree algos): 2 x part_stride
+  Pad* pad[kMaxRanks];
+  volatile uint32_t* err;  // host-mapped error word (hfr_status_t), 0 = ok
+  uint64_t count;          // elements per rank
+  uint64_t epoch;
+  uint64_t sig;            // hash of the call's arguments, compared across ranks
+  uint64_t timeout_ns;
+  uint64_t part_stride;    // floats per partial slot
+  uint64_t half_base[2];   // tree algos: element offset of the range each parity works on
+  uint64_t half_len[2];
+  uint32_t c_lo, c_hi;     // tree algos: global chunk range of this launch
+  float scale;
+  int n;                   // ranks in the comm
+  int rank0;               // rank of blockIdx.y == 0
+  int chunk;               // tree chunk elements (multiple of 256)
+  int ntree;               // nodes per tree (n, or n/2 for PAIR)
+  TreeNode tree[2][kMaxRanks];
+};
+
+// ---------------------------------------------------------------------------
+// memory-model primitives (PTX ISA memory consistency model, sys scope)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// 128-bit data movement.  Loads skip L1 allocation (each byte is read once);
+// peer addresses bypass the local L2 in hardware.
+__device__ __forceinline__ uint4 ld128(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st128(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// status codes mirrored from include/hfr.h
+constexpr uint32_t kErrProtocol = 5;
+constexpr uint32_t kErrTimeout = 6;
+
+__device__ __forceinline__ void raise_error(const Args& a, uint32_t code) {
+  if (*a.err == 0) *a.err = code;
+}
+
+// Spin until *p >= target.  Returns false on timeout or if another CTA
+// already raised an error (checked every 1024 polls).
+__device__ __noinline__ bool wait_ge(const Args& a, const uint64_t* p, uint64_t target) {
+  if (ld_acquire_sys(p) >= target) return true;
+  uint64_t t0 = globaltimer();
+  for (uint32_t it = 1;; ++it) {
+    if (ld_acquire_sys(p) >= target) return true;
+    if ((it & 1023u) == 0) {
+      if (*a.err != 0) return false;
+      if (globaltimer() - t0 > a.timeout_ns) {
+        raise_error(a, kErrTimeout);
+        return false;
+      }
+    }
+  }
+}
+
+// a0 "trigger and entry handshake" ("wait for chunk-i
+// transfer finished in this node", made a device barrier): CTA b of `rank`
+// publishes (sig, epoch) to CTA b of every rank and waits for all of them.
+// When it returns true every rank has entered this launch, so every rank's
+// prior stream work on its buffers is complete.  Caller must __syncthreads().
+__device__ __forceinline__ bool entry_barrier(const Args& a, int rank, int b) {
+  bool ok = true;
+  const int q = threadIdx.x;
+  if (q < a.n) {
+    st_relaxed_sys(&a.pad[q]->sig[b][rank], a.sig);
+    st_release_sys(&a.pad[q]->entry[b][rank], a.epoch);
+    ok = wait_ge(a, &a.pad[rank]->entry[b][q], a.epoch);
+    if (ok && ld_relaxed_sys(&a.pad[rank]->sig[b][q]) != a.sig) {
+      raise_error(a, kErrProtocol);
+      ok = false;
+    }
+  }
+  return __syncthreads_and(ok);
+}
+
+// a5 completion: CTA b tells CTA b of every rank that all its loads from and
+// stores to that rank are done, and waits for the same from everyone.
+__device__ __forceinline__ void exit_barrier(const Args& a, int rank, int b) {
+  __syncthreads();
+  const int q = threadIdx.x;
+  if (q < a.n) {
+    fence_acq_rel_sys();
+    st_relaxed_sys(&a.pad[q]->exit[b][rank], a.epoch);
+    wait_ge(a, &a.pad[rank]->exit[b][q], a.epoch);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// element types
+// ---------------------------------------------------------------------------
+struct F32 {
+  using T = float;
+  static constexpr int kPerVec = 4;  // elements per 16 B
+  __device__ static __forceinline__ void widen(const uint4& v, float* f) {
+    f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
+    f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+  }
+  __device__ static __forceinline__ uint4 narrow(const float* f) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+  }
+  __device__ static __forceinline__ float load1(const char* p, uint64_t i) {
+    return reinterpret_cast<const float*>(p)[i];
+  }
+  __device__ static __forceinline__ void store1(char* p, uint64_t i, float v) {
+    reinterpret_cast<float*>(p)[i] = v;
+  }
+};
+
+struct BF16 {
+  using T = __nv_bfloat16;
+  static constexpr int kPerVec = 8;
+  __device__ static __forceinline__ void widen(const uint4& v, float* f) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      f[2 * j] = __uint_as_float(w[j] << 16);
+      f[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+    }
+  }
+  __device__ static __forceinline__ uint32_t rne(float x) {
+    return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(x));
+  }
+  __device__ static __forceinline__ uint4 narrow(const float* f) {
+    return make_uint4(rne(f[0]) | (rne(f[1]) << 16), rne(f[2]) | (rne(f[3]) << 16),
+                      rne(f[4]) | (rne(f[5]) << 16), rne(f[6]) | (rne(f[7]) << 16));
+  }
+  __device__ static __forceinline__ float load1(const char* p, uint64_t i) {
+    return __uint_as_float(((uint32_t)reinterpret_cast<const uint16_t*>(p)[i]) << 16);
+  }
+  __device__ static __forceinline__ void store1(char* p, uint64_t i, float v) {
+    reinterpret_cast<uint16_t*>(p)[i] = (uint16_t)rne(v);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Subsystems (1)+(3), FLAT: fused reduce-scatter + all-gather/cast/scale.
+//
+// Rank g owns shard g = vectors [g*V/n, (g+1)*V/n).  For each vector of its
+// shard a thread loads the 16 B at that offset from all n ranks' buffers
+// (n-1 over NVLink; Algorithm 1's D2H + "Dc_i += GPU-j's Dc_i", PAPER.md:
+// 327-336), folds them serially in rank order 0..n-1 in fp32 (lanes split
+// ELEMENTS, never ranks, so the order is the oracle's), multiplies by scale
+// once, casts, and stores the result to all n buffers (Algorithm 2 pass 2 /
+// H2D fan-out).  In place without a mid-kernel barrier:
+// shard g of rank q's buffer is read and then written only by rank g.
+// ---------------------------------------------------------------------------
+template <class E, int NR, int U>
+__device__ __forceinline__ void flat_vecs(const Args& a, uint64_t i, uint64_t stride, uint64_t hi) {
+  // U vectors per thread, all U*NR loads issued before the first fold so that
+  // U*NR 16-byte NVLink reads are in flight per thread.
+  constexpr int K = E::kPerVec;
+  uint4 v[U][NR];
+  bool ok[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) ok[u] = i + u * stride < hi;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (ok[u]) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r) v[u][r] = ld128(a.buf[r] + (i + u * stride) * 16);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (ok[u]) {
+      float acc[K];
+      E::widen(v[u][0], acc);
+#pragma unroll
+      for (int r = 1; r < NR; ++r) {
+        float t[K];
+        E::widen(v[u][r], t);
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = __fadd_rn(acc[k], t[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[k] = __fmul_rn(acc[k], a.scale);
+      const uint4 o = E::narrow(acc);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) st128(a.buf[r] + (i + u * stride) * 16, o);
+    }
+  }
+}
+
+template <class E>
+__device__ __forceinline__ void flat_vec_dyn(const Args& a, const int n, uint64_t i) {
+  constexpr int K = E::kPerVec;
+  float acc[K];
+  E::widen(ld128(a.buf[0] + i * 16), acc);
+  for (int r = 1; r < n; ++r) {
+    float t[K];
+    E::widen(ld128(a.buf[r] + i * 16), t);
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = __fadd_rn(acc[k], t[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = __fmul_rn(acc[k], a.scale);
+  const uint4 o = E::narrow(acc);
+  for (int r = 0; r < n; ++r) st128(a.buf[r] + i * 16, o);
+}
+
+// NR = compile-time rank count (1..8), 0 = runtime a.n (up to kMaxRanks).
+template <class E, int NR>
+__global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
+  const int rank = a.rank0 + blockIdx.y;
+  const int n = NR > 0 ? NR : a.n;
+  const int b = blockIdx.x;
+  if (entry_barrier(a, rank, b)) {
+    constexpr int K = E::kPerVec;
+    constexpr int U = NR > 4 ? 2 : (NR > 2 ? 3 : 4);
+    const uint64_t nvec = a.count / K;
+    const uint64_t lo = nvec * rank / n, hi = nvec * (rank + 1) / n;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    if constexpr (NR > 0) {
+      for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += U * stride)
+        flat_vecs<E, NR, U>(a, i, stride, hi);
+    } else {
+      for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += stride)
+        flat_vec_dyn<E>(a, n, i);
+    }
+    // ragged tail (< K elements) — owned by the last rank, CTA 0
+    const uint64_t t0 = nvec * K;
+    if (rank == n - 1 && b == 0 && threadIdx.x < a.count - t0) {
+      const uint64_t e = t0 + threadIdx.x;
+      float acc = E::load1(a.buf[0], e);
+      for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, E::load1(a.buf[r], e));
+      acc = __fmul_rn(acc, a.scale);
+      for (int r = 0; r < n; ++r) E::store1(a.buf[r], e, acc);
+    }
+  }
+  exit_barrier(a, rank, b);
+}
+
+// ---------------------------------------------------------------------------
+// Subsystem (2): double binary tree (Algorithm 2) as a
+// push-only P2P schedule, and (PAIR) "HFReduce with NVLink".
+//
+// Chunk c (global index within the half) rides tree c & 1 (reading R8).  Up
+// pass (Alg. 2 pass 1, "DL_i += DR_i"): a node waits for its children's fp32
+// partials (pushed into its own partial slots), combines them in-order with
+// its own value (reading R10) and pushes the result into its parent's slot;
+// the root scales, casts, writes the final chunk to its own buffer and pushes
+// it to its children.  Down pass (Alg. 2 pass 2): a node waits for the final
+// chunk from its parent and forwards it to its children.  PAIR: tree nodes
+// are pairs k = (2k, 2k+1); member 2k+h works on half h, its node value is
+// fl32(x_2k + x_2k+1) (the NVLink pair pre-reduce, fused), and every final
+// chunk is also pushed to the partner (the pair all-gather, fused).
+// Every NVLink transfer is a remote store; all loads are local except the
+// partner's half in PAIR mode.
+// ---------------------------------------------------------------------------
+template <class E>
+__device__ __forceinline__ void load8(const char* base, uint64_t e, float* f) {
+  // 8 consecutive elements starting at element e (e % 8 == 0)
+  if constexpr (E::kPerVec == 8) {
+    E::widen(ld128(base + e * 2), f);
+  } else {
+    E::widen(ld128(base + e * 4), f);
+    E::widen(ld128(base + e * 4 + 16), f + 4);
+  }
+}
+template <class E>
+__device__ __forceinline__ void store8(char* base, uint64_t e, const float* f) {
+  if constexpr (E::kPerVec == 8) {
+    st128(base + e * 2, E::narrow(f));
+  } else {
+    st128(base + e * 4, E::narrow(f));
+    st128(base + e * 4 + 16, E::narrow(f + 4));
+  }
+}
+__device__ __forceinline__ void load8_f32(const float* base, uint64_t e, float* f) {
+  F32::widen(ld128(base + e), f);
+  F32::widen(ld128(base + e + 4), f + 4);
+}
+__device__ __forceinline__ void store8_f32(float* base, uint64_t e, const float* f) {
+  st128(base + e, F32::narrow(f));
+  st128(base + e + 4, F32::narrow(f + 4));
+}
+
+template <class E, bool PAIR>
+__global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
+  const int rank = a.rank0 + blockIdx.y;
+  const int b = blockIdx.x;
+  const bool ok = entry_barrier(a, rank, b);
+  if (!ok) return;
+
+  const int h = PAIR ? (rank & 1) : 0;
+  const int me = PAIR ? (rank >> 1) : rank;
+  const int partner = rank ^ 1;
+  const uint64_t base = a.half_base[h], len = a.half_len[h];
+  const uint64_t C = (uint64_t)a.chunk;
+  const uint64_t nch = (len + C - 1) / C;
+  const uint64_t c_end = nch < a.c_hi ? nch : a.c_hi;
+  Pad* const mypad = a.pad[rank];
+  char* const mybuf = a.buf[rank];
+  const float* const mypart = a.part[rank];
+  auto member = [&](int node) { return PAIR ? 2 * node + h : node; };
+
+  // ---- up pass -----------------------------------------------------------
+  for (uint64_t c = a.c_lo + b; c < c_end; c += gridDim.x) {
+    const TreeNode nd = a.tree[c & 1][me];
+    const uint32_t lc = (uint32_t)(c - a.c_lo);
+    bool got = true;
+    if (threadIdx.x < nd.nchild) got = wait_ge(a, &mypad->up[threadIdx.x][lc], a.epoch);
+    if (!__syncthreads_and(got)) return;
+
+    const uint64_t e0 = c * C, e1 = (e0 + C < len) ? e0 + C : len;  // offsets within the half
+    const uint64_t nv = (e1 - e0) / 8;
+    const bool root = nd.parent < 0;
+    char* const pbuf = PAIR ? a.buf[partner] : nullptr;
+    float* const dst_part = root ? nullptr : a.part[member(nd.parent)] + (uint64_t)nd.slot * a.part_stride;
+    for (uint64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+      const uint64_t e = e0 + v * 8;
+      float acc[8], t[8];
+      // node value x_v (PAIR: fl32(x_2k + x_2k+1), lower rank first)
+      float xv[8];
+      load8<E>(mybuf, base + e, xv);
+      if constexpr (PAIR) {
+        float xp[8];
+        load8<E>(pbuf, base + e, xp);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) xv[k] = h == 0 ? __fadd_rn(xv[k], xp[k]) : __fadd_rn(xp[k], xv[k]);
+      }
+      // in-order combination: children below, x_v, children above
+      if (nd.self_pos == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = xv[j];
+      } else {
+        load8_f32(mypart, e, acc);
+      }
+      for (int k = 1; k <= nd.nchild; ++k) {
+        if (k == nd.self_pos) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], xv[j]);
+        } else {
+          load8_f32(mypart + (uint64_t)(k < nd.self_pos ? k : k - 1) * a.part_stride, e, t);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], t[j]);
+        }
+      }
+      if (root) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = __fmul_rn(acc[j], a.scale);
+        store8<E>(mybuf, base + e, acc);
+        for (int k = 0; k < nd.nchild; ++k) store8<E>(a.buf[member(nd.child[k])], base + e, acc);
+        if constexpr (PAIR) store8<E>(pbuf, base + e, acc);
+      } else {
+        store8_f32(dst_part, e, acc);
+      }
+    }
+    // ragged tail of the half (only the last chunk can have one)
+    for (uint64_t e = e0 + nv * 8 + threadIdx.x; e < e1; e += blockDim.x) {
+      float xv = E::load1(mybuf, base + e);
+      if constexpr (PAIR) {
+        const float xp = E::load1(pbuf, base + e);
+        xv = h == 0 ? __fadd_rn(xv, xp) : __fadd_rn(xp, xv);
+      }
+      float acc = 0.f;
+      for (int k = 0; k <= nd.nchild; ++k) {
+        const float s = k == nd.self_pos ? xv : mypart[(uint64_t)(k < nd.self_pos ? k : k - 1) * a.part_stride + e];
+        acc = k == 0 ? s : __fadd_rn(acc, s);
+      }
+      if (root) {
+        acc = __fmul_rn(acc, a.scale);
+        E::store1(mybuf, base + e, acc);
+        for (int k = 0; k < nd.nchild; ++k) E::store1(a.buf[member(nd.child[k])], base + e, acc);
+        if constexpr (PAIR) E::store1(pbuf, base + e, acc);
+      } else {
+        dst_part[e] = acc;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_acq_rel_sys();
+      if (root) {
+        for (int k = 0; k < nd.nchild; ++k) st_relaxed_sys(&a.pad[member(nd.child[k])]->down[lc], a.epoch);
+        if constexpr (PAIR) st_relaxed_sys(&a.pad[partner]->pdown[lc], a.epoch);
+      } else {
+        st_relaxed_sys(&a.pad[member(nd.parent)]->up[nd.slot][lc], a.epoch);
+      }
+    }
+  }
+
+  // ---- down pass ---------------------------------------------------------
+  for (uint64_t c = a.c_lo + b; c < c_end; c += gridDim.x) {
+    const TreeNode nd = a.tree[c & 1][me];
+    if (nd.parent < 0) continue;  // the root already pushed its final chunk
+    const uint32_t lc = (uint32_t)(c - a.c_lo);
+    bool got = true;
+    if (threadIdx.x == 0) got = wait_ge(a, &mypad->down[lc], a.epoch);
+    if (!__syncthreads_and(got)) return;
+    if (nd.nchild == 0 && !PAIR) continue;
+    const uint64_t e0 = c * C, e1 = (e0 + C < len) ? e0 + C : len;
+    const int esz = (int)sizeof(typename E::T);
+    const uint64_t b0 = (base + e0) * esz, b1 = (base + e1) * esz;  // byte range
+    const uint64_t nv = (b1 - b0) / 16;
+    for (uint64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+      const uint4 val = ld128(mybuf + b0 + v * 16);
+      for (int k = 0; k < nd.nchild; ++k) st128(a.buf[member(nd.child[k])] + b0 + v * 16, val);
+      if constexpr (PAIR) st128(a.buf[partner] + b0 + v * 16, val);
+    }
+    for (uint64_t y = b0 + nv * 16 + threadIdx.x * esz; y < b1; y += (uint64_t)blockDim.x * esz) {
+      if (esz == 2) {
+        const uint16_t val = *reinterpret_cast<const uint16_t*>(mybuf + y);
+        for (int k = 0; k < nd.nchild; ++k) *reinterpret_cast<uint16_t*>(a.buf[member(nd.child[k])] + y) = val;
+        if constexpr (PAIR) *reinterpret_cast<uint16_t*>(a.buf[partner] + y) = val;
+      } else {
+        const uint32_t val = *reinterpret_cast<const uint32_t*>(mybuf + y);
+        for (int k = 0; k < nd.nchild; ++k) *reinterpret_cast<uint32_t*>(a.buf[member(nd.child[k])] + y) = val;
+        if constexpr (PAIR) *reinterpret_cast<uint32_t*>(a.buf[partner] + y) = val;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_acq_rel_sys();
+      for (int k = 0; k < nd.nchild; ++k) st_relaxed_sys(&a.pad[member(nd.child[k])]->down[lc], a.epoch);
+      if constexpr (PAIR) st_relaxed_sys(&a.pad[partner]->pdown[lc], a.epoch);
+    }
+  }
+
+  // ---- PAIR: wait until the partner's half has fully landed in my buffer ---
+  if constexpr (PAIR) {
+    const uint64_t olen = a.half_len[h ^ 1];
+    const uint64_t onch = (olen + C - 1) / C;
+    const uint64_t oend = onch < a.c_hi ? onch : a.c_hi;
+    for (uint64_t c = a.c_lo + b; c < oend; c += gridDim.x) {
+      if (threadIdx.x == 0) wait_ge(a, &mypad->pdown[(uint32_t)(c - a.c_lo)], a.epoch);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Staging copy (buffers outside peer-mapped memory) and the device barrier.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) hfr_copy_kernel(char* dst, const char* src, uint64_t bytes) {
+  const uint64_t nv = bytes / 16;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  if (aligned) {
+    for (uint64_t i = tid; i < nv; i += stride) st128(dst + i * 16, ld128(src + i * 16));
+    for (uint64_t i = nv * 16 + tid; i < bytes; i += stride) dst[i] = src[i];
+  } else {
+    for (uint64_t i = tid; i < bytes; i += stride) dst[i] = src[i];
+  }
+}
+
+__global__ void hfr_barrier_kernel(const Args a) {
+  const int rank = a.rank0 + blockIdx.y;
+  entry_barrier(a, rank, 0);
+}
+
+}  // namespace hfr

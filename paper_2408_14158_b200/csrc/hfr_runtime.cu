@@ -1,0 +1,850 @@
+// hfr_runtime.cu — host runtime and C ABI (include/hfr.h) of the B200-native
+// HFReduce (arXiv 2408.14158 §4).
+//
+// Responsibilities: communicator setup (peer-mapped signal pad + scratch,
+// CUDA IPC handle exchange through the caller's all-gather callback), the
+// symmetric-memory region table (zero-copy buffers), the chunk/segment plan
+// (Alg. 1 "Split Dg by Chunk_Size"), the double-binary-tree
+// tables (reading R9), argument signatures for the cross-rank protocol check,
+// stream/event plumbing for asynchronous calls, and the
+// sticky error state.  All data movement and arithmetic happens in the
+// kernels of hfr_kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hfr.h"
+#include "hfr_kernels.cuh"
+
+using namespace hfr;
+
+namespace {
+
+thread_local std::string g_cuda_error;
+
+void note_cuda(cudaError_t e, const char* what) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "%s: %s (%d)", what, cudaGetErrorString(e), (int)e);
+  g_cuda_error = buf;
+}
+
+#define HFR_CU(call)                                                               \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess) {                                                       \
+      note_cuda(e_, #call);                                                        \
+      return e_ == cudaErrorMemoryAllocation ? HFR_ERR_OUT_OF_MEMORY : HFR_ERR_CUDA; \
+    }                                                                              \
+  } while (0)
+
+#define HFR_TRY(expr)                 \
+  do {                                \
+    hfr_status_t s_ = (expr);         \
+    if (s_ != HFR_SUCCESS) return s_; \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+constexpr size_t kAlign = 256;
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// One peer-mapped allocation: base[r] is rank r's copy as addressable from
+// this process (own allocation for local ranks, IPC mapping for peers).
+struct Region {
+  char* base[kMaxRanks] = {};
+  bool opened[kMaxRanks] = {};  // base[r] came from cudaIpcOpenMemHandle
+  bool owned = false;           // we cudaMalloc'ed base[local ranks]
+  size_t bytes = 0;
+};
+
+struct IpcRecord {
+  cudaIpcMemHandle_t handle;
+  uint64_t offset;  // byte offset of the exported pointer inside its allocation
+  uint64_t bytes;
+  int32_t device;
+  int32_t rank;
+};
+
+}  // namespace
+
+struct hfr_req_s {
+  cudaEvent_t ev = nullptr;
+  hfr_comm_s* comm = nullptr;
+};
+
+struct hfr_comm_s {
+  int rank = 0, n = 1, dev = 0, local = 1;
+  bool virt = false;
+  hfr_config_t cfg{};
+  hfr_allgather_fn ag = nullptr;
+  void* ctx = nullptr;
+  Region pad;       // Pad per rank
+  Region scratch;   // staging + tree partials per rank
+  std::vector<Region> regions;  // hfr_mem_alloc / hfr_register memory
+  uint64_t epoch = 0;
+  uint32_t* err_host = nullptr;  // host-mapped error word
+  uint32_t* err_dev = nullptr;
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev_pool;
+  int num_sms = 148;
+  hfr_status_t sticky = HFR_SUCCESS;
+  uint64_t launches = 0;
+};
+
+// ---------------------------------------------------------------------------
+// double binary tree (reading R9).  Independent of oracle/: tree A is built
+// top-down from the CHILD rules (the oracle derives it from parent rules).
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kMaxTreeN = kMaxRanks * 64;  // hfr_tree_query supports n <= 1024
+
+void build_tree(int n, int which, int* parent, std::array<int, 2>* child, int* nchild) {
+  std::vector<int> pa(n, -1);
+  std::vector<std::vector<int>> ch(n);
+  if (n > 1) {
+    int top = 1;
+    while (top * 2 < n) top *= 2;
+    ch[0].push_back(top);
+    for (int r = 1; r < n; ++r) {
+      const int b = r & -r;
+      if (b > 1) {
+        ch[r].push_back(r - b / 2);
+        int h = b / 2;
+        while (h > 0 && r + h >= n) h /= 2;
+        if (h > 0) ch[r].push_back(r + h);
+      }
+    }
+    for (int r = 0; r < n; ++r)
+      for (int c : ch[r]) pa[c] = r;
+  }
+  // tree B: relabel by mirror (even n) or shift (odd n)
+  auto f = [&](int r) { return which == 0 ? r : (n % 2 == 0 ? n - 1 - r : (r + 1) % n); };
+  for (int r = 0; r < n; ++r) {
+    nchild[r] = 0;
+    child[r][0] = child[r][1] = -1;
+  }
+  for (int r = 0; r < n; ++r) parent[f(r)] = pa[r] < 0 ? -1 : f(pa[r]);
+  for (int r = 0; r < n; ++r) {
+    const int p = parent[r];
+    if (p >= 0) child[p][nchild[p]++] = r;
+  }
+  for (int r = 0; r < n; ++r)
+    if (nchild[r] == 2 && child[r][0] > child[r][1]) std::swap(child[r][0], child[r][1]);
+}
+
+void fill_tree_nodes(int m, TreeNode (*out)[kMaxRanks]) {
+  for (int which = 0; which < 2; ++which) {
+    int parent[kMaxRanks], nchild[kMaxRanks];
+    std::array<int, 2> child[kMaxRanks];
+    build_tree(m, which, parent, child, nchild);
+    for (int v = 0; v < m; ++v) {
+      TreeNode& t = out[which][v];
+      t.parent = (int8_t)parent[v];
+      t.nchild = (int8_t)nchild[v];
+      t.child[0] = (int8_t)child[v][0];
+      t.child[1] = (int8_t)child[v][1];
+      int below = 0;
+      for (int k = 0; k < nchild[v]; ++k) below += child[v][k] < v;
+      t.self_pos = (int8_t)below;
+      t.slot = 0;
+      if (parent[v] >= 0) {
+        const int p = parent[v];
+        t.slot = (int8_t)(child[p][0] == v ? 0 : 1);
+      }
+    }
+  }
+}
+
+// pair split (reading R13): H = min(N, 256 * ceil(N / 512))
+uint64_t pair_half(uint64_t count) {
+  const uint64_t h = 256 * ((count + 511) / 512);
+  return h < count ? h : count;
+}
+
+uint64_t fnv(uint64_t h, uint64_t v) {
+  for (int i = 0; i < 8; ++i) {
+    h ^= (v >> (8 * i)) & 0xFF;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+size_t dtype_size(hfr_dtype_t t) { return t == HFR_BFLOAT16 ? 2 : 4; }
+
+int effective_algo(const hfr_comm_s* c) { return c->cfg.algo == HFR_ALGO_AUTO ? HFR_ALGO_FLAT : c->cfg.algo; }
+
+hfr_status_t validate_cfg(const hfr_config_t& c) {
+  if (c.algo < HFR_ALGO_AUTO || c.algo > HFR_ALGO_PAIR_DBT) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.chunk_elems % 256 != 0 || c.chunk_elems > (1u << 30)) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.max_ctas < 0 || c.max_ctas > kMaxCtas) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.threads != 0 && (c.threads < 128 || c.threads > 512 || c.threads % 32 != 0)) return HFR_ERR_INVALID_ARGUMENT;
+  if (!(c.scale == c.scale)) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.timeout_ms < 0) return HFR_ERR_INVALID_ARGUMENT;
+  return HFR_SUCCESS;
+}
+
+void resolve_defaults(hfr_config_t& c) {
+  if (c.chunk_elems == 0) c.chunk_elems = 8192;
+  if (c.threads == 0) c.threads = 512;
+  if (c.scratch_bytes == 0) c.scratch_bytes = 256ull << 20;
+  if (c.timeout_ms == 0) c.timeout_ms = 60000;
+}
+
+// ---------------------------------------------------------------------------
+// collective region setup
+// ---------------------------------------------------------------------------
+hfr_status_t exchange(hfr_comm_s* c, const void* send, void* recv, size_t bytes) {
+  if (c->n == 1 || c->virt) {
+    memcpy(recv, send, bytes);
+    return HFR_SUCCESS;
+  }
+  if (c->ag(send, recv, bytes, c->ctx) != 0) return HFR_ERR_INTERNAL;
+  return HFR_SUCCESS;
+}
+
+// Export [ptr, ptr+bytes) of THIS rank (real comms) and open every peer's.
+hfr_status_t share_region(hfr_comm_s* c, char* ptr, size_t bytes, Region* out) {
+  if (c->virt) return HFR_ERR_INTERNAL;
+  IpcRecord mine{};
+  mine.rank = c->rank;
+  mine.device = c->dev;
+  mine.bytes = bytes;
+  if (c->n > 1) {
+    // Export the allocation containing ptr (cudaIpcGetMemHandle wants a base).
+    void* base = ptr;
+    size_t range = 0;
+    typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
+    static GetRange get_range = nullptr;
+    if (!get_range) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        get_range = (GetRange)fn;
+    }
+    if (get_range) {
+      unsigned long long b = 0;
+      if (get_range(&b, &range, (unsigned long long)ptr) == 0) base = (void*)b;
+    }
+    mine.offset = (uint64_t)(ptr - (char*)base);
+    HFR_CU(cudaIpcGetMemHandle(&mine.handle, base));
+  }
+  std::vector<IpcRecord> all(c->n);
+  HFR_TRY(exchange(c, &mine, all.data(), sizeof(IpcRecord)));
+  Region r;
+  r.bytes = bytes;
+  for (int q = 0; q < c->n; ++q) {
+    if (all[q].rank != q || all[q].bytes != bytes) {
+      for (int k = 0; k < q; ++k)
+        if (r.opened[k]) cudaIpcCloseMemHandle(r.base[k] - all[k].offset);
+      return HFR_ERR_PROTOCOL;
+    }
+    if (q == c->rank) {
+      r.base[q] = ptr;
+      continue;
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, all[q].handle, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      note_cuda(e, "cudaIpcOpenMemHandle");
+      for (int k = 0; k < q; ++k)
+        if (r.opened[k]) cudaIpcCloseMemHandle(r.base[k] - all[k].offset);
+      return HFR_ERR_CUDA;
+    }
+    r.base[q] = (char*)p + all[q].offset;
+    r.opened[q] = true;
+  }
+  *out = r;
+  return HFR_SUCCESS;
+}
+
+void close_region(hfr_comm_s* c, Region& r) {
+  for (int q = 0; q < c->n; ++q) {
+    if (r.opened[q] && r.base[q]) {
+      // the mapping was opened at the allocation base; recover it
+      void* b = r.base[q];
+      typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
+      cudaDriverEntryPointQueryResult qr;
+      void* fn = nullptr;
+      if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
+          qr == cudaDriverEntryPointSuccess) {
+        unsigned long long base = 0;
+        size_t sz = 0;
+        if (((GetRange)fn)(&base, &sz, (unsigned long long)r.base[q]) == 0) b = (void*)base;
+      }
+      cudaIpcCloseMemHandle(b);
+    }
+    r.opened[q] = false;
+  }
+  if (r.owned) {
+    const int lo = c->virt ? 0 : c->rank, hi = c->virt ? c->n : c->rank + 1;
+    for (int q = lo; q < hi; ++q)
+      if (r.base[q]) cudaFree(r.base[q]);
+  }
+  r = Region();
+}
+
+// Allocate `bytes` on every local rank (zeroed) and make it peer-visible.
+hfr_status_t alloc_region(hfr_comm_s* c, size_t bytes, Region* out) {
+  bytes = round_up(std::max<size_t>(bytes, kAlign), 2u << 20);
+  Region r;
+  r.bytes = bytes;
+  r.owned = true;
+  if (c->virt) {
+    for (int q = 0; q < c->n; ++q) {
+      void* p = nullptr;
+      cudaError_t e = cudaMalloc(&p, bytes);
+      if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);
+      if (e != cudaSuccess) {
+        note_cuda(e, "cudaMalloc");
+        for (int k = 0; k < q; ++k) cudaFree(r.base[k]);
+        return e == cudaErrorMemoryAllocation ? HFR_ERR_OUT_OF_MEMORY : HFR_ERR_CUDA;
+      }
+      r.base[q] = (char*)p;
+    }
+    HFR_CU(cudaDeviceSynchronize());
+    *out = r;
+    return HFR_SUCCESS;
+  }
+  void* p = nullptr;
+  HFR_CU(cudaMalloc(&p, bytes));
+  cudaError_t e = cudaMemset(p, 0, bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();  // zeroed before any peer can see it
+  if (e != cudaSuccess) {
+    note_cuda(e, "cudaMemset");
+    cudaFree(p);
+    return HFR_ERR_CUDA;
+  }
+  hfr_status_t s = share_region(c, (char*)p, bytes, &r);
+  if (s != HFR_SUCCESS) {
+    cudaFree(p);
+    return s;
+  }
+  r.owned = true;
+  *out = r;
+  return HFR_SUCCESS;
+}
+
+hfr_status_t common_init(hfr_comm_s* c) {
+  HFR_CU(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->dev));
+  HFR_CU(cudaHostAlloc((void**)&c->err_host, sizeof(uint32_t) * 4, cudaHostAllocMapped | cudaHostAllocPortable));
+  *c->err_host = 0;
+  HFR_CU(cudaHostGetDevicePointer((void**)&c->err_dev, c->err_host, 0));
+  int lo = 0, hi = 0;
+  HFR_CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  HFR_CU(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+  HFR_TRY(alloc_region(c, sizeof(Pad), &c->pad));
+  HFR_TRY(alloc_region(c, c->cfg.scratch_bytes, &c->scratch));
+  return HFR_SUCCESS;
+}
+
+// Scratch must hold a staged copy of the message plus the tree partials.
+// Depends only on (count, dtype, algo) so every rank grows in lockstep.
+size_t scratch_need(const hfr_comm_s* c, size_t count, hfr_dtype_t dt, int algo) {
+  size_t need = round_up(count * dtype_size(dt), kAlign);
+  if (algo == HFR_ALGO_DBT) need += 2 * round_up(count, 64) * 4;
+  if (algo == HFR_ALGO_PAIR_DBT) need += 2 * round_up(pair_half(count), 64) * 4;
+  (void)c;
+  return need;
+}
+
+hfr_status_t ensure_scratch(hfr_comm_s* c, size_t need) {
+  if (need <= c->scratch.bytes) return HFR_SUCCESS;
+  // collective growth: drain our device so no kernel of ours still touches
+  // the old scratch, swap, then release the old mappings.
+  HFR_CU(cudaDeviceSynchronize());
+  Region fresh;
+  HFR_TRY(alloc_region(c, std::max(need, c->scratch.bytes * 2), &fresh));
+  close_region(c, c->scratch);
+  c->scratch = fresh;
+  return HFR_SUCCESS;
+}
+
+// ---------------------------------------------------------------------------
+// launches
+// ---------------------------------------------------------------------------
+template <class E>
+const void* flat_fn(int n) {
+  switch (n) {
+    case 1: return (const void*)hfr_flat_kernel<E, 1>;
+    case 2: return (const void*)hfr_flat_kernel<E, 2>;
+    case 3: return (const void*)hfr_flat_kernel<E, 3>;
+    case 4: return (const void*)hfr_flat_kernel<E, 4>;
+    case 5: return (const void*)hfr_flat_kernel<E, 5>;
+    case 6: return (const void*)hfr_flat_kernel<E, 6>;
+    case 7: return (const void*)hfr_flat_kernel<E, 7>;
+    case 8: return (const void*)hfr_flat_kernel<E, 8>;
+    default: return (const void*)hfr_flat_kernel<E, 0>;
+  }
+}
+
+template <class E>
+const void* tree_fn(bool pair) {
+  return pair ? (const void*)hfr_tree_kernel<E, true> : (const void*)hfr_tree_kernel<E, false>;
+}
+
+hfr_status_t launch(hfr_comm_s* c, const void* fn, int grid_x, int threads, Args& a, cudaStream_t s) {
+  a.epoch = ++c->epoch;
+  void* params[] = {&a};
+  dim3 grid(grid_x, c->local), block(threads);
+  cudaError_t e;
+  if (c->virt && c->local > 1) {
+    e = cudaLaunchCooperativeKernel(fn, grid, block, params, 0, s);
+  } else {
+    e = cudaLaunchKernel(fn, grid, block, params, 0, s);
+  }
+  if (e != cudaSuccess) {
+    note_cuda(e, "launch");
+    return HFR_ERR_CUDA;
+  }
+  ++c->launches;
+  return HFR_SUCCESS;
+}
+
+// CTAs per rank: the config cap (default one per SM), limited so that all
+// ranks' CTAs of a virtual comm are co-resident (cooperative launch).
+hfr_status_t ctas_per_rank(hfr_comm_s* c, const void* fn, int threads, int want, int* out) {
+  int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : c->num_sms;
+  g = std::min(g, kMaxCtas);
+  if (want > 0) g = std::min(g, want);
+  if (c->virt && c->local > 1) {
+    int occ = 0;
+    HFR_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0));
+    const int cap = occ * c->num_sms / c->local;
+    if (cap < 1) return HFR_ERR_UNSUPPORTED;
+    g = std::min(g, cap);
+  }
+  *out = std::max(g, 1);
+  return HFR_SUCCESS;
+}
+
+void base_args(hfr_comm_s* c, Args& a, uint64_t count, uint64_t sig) {
+  memset(&a, 0, sizeof a);
+  for (int q = 0; q < c->n; ++q) a.pad[q] = reinterpret_cast<Pad*>(c->pad.base[q]);
+  a.err = c->err_dev;
+  a.count = count;
+  a.sig = sig;
+  a.timeout_ns = (uint64_t)c->cfg.timeout_ms * 1000000ull;
+  a.scale = c->cfg.scale;
+  a.n = c->n;
+  a.rank0 = c->virt ? 0 : c->rank;
+}
+
+hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
+                      cudaStream_t s) {
+  const void* fn = dt == HFR_BFLOAT16 ? flat_fn<BF16>(c->n) : flat_fn<F32>(c->n);
+  const int threads = c->cfg.threads;
+  const uint64_t per = dt == HFR_BFLOAT16 ? 8 : 4;
+  const uint64_t vec_per_rank = count / per / c->n + 1;
+  int g = 0;
+  HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>((vec_per_rank + threads - 1) / threads, kMaxCtas), &g));
+  Args a;
+  base_args(c, a, count, fnv(sig, (uint64_t)g * 1315423911ull + threads));
+  for (int q = 0; q < c->n; ++q) a.buf[q] = bufs[q];
+  return launch(c, fn, g, threads, a, s);
+}
+
+hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, bool pair, uint64_t sig,
+                      cudaStream_t s) {
+  const void* fn = dt == HFR_BFLOAT16 ? tree_fn<BF16>(pair) : tree_fn<F32>(pair);
+  const int threads = c->cfg.threads;
+  const uint64_t C = c->cfg.chunk_elems;
+  Args a;
+  base_args(c, a, count, 0);
+  const size_t stage = round_up(count * dtype_size(dt), kAlign);
+  if (pair) {
+    const uint64_t H = pair_half(count);
+    a.half_base[0] = 0;
+    a.half_len[0] = H;
+    a.half_base[1] = H;
+    a.half_len[1] = count - H;
+    a.part_stride = round_up(H, 64);
+    a.ntree = c->n / 2;
+  } else {
+    a.half_base[0] = a.half_base[1] = 0;
+    a.half_len[0] = a.half_len[1] = count;
+    a.part_stride = round_up(count, 64);
+    a.ntree = c->n;
+  }
+  fill_tree_nodes(a.ntree, a.tree);
+  a.chunk = (int)C;
+  for (int q = 0; q < c->n; ++q) {
+    a.buf[q] = bufs[q];
+    a.part[q] = reinterpret_cast<float*>(c->scratch.base[q] + stage);
+  }
+  const uint64_t nch = (a.half_len[0] + C - 1) / C;  // half 0 is the longer one
+  for (uint64_t lo = 0; lo < std::max<uint64_t>(nch, 1); lo += kMaxChunks) {
+    const uint64_t hi = lo + kMaxChunks;
+    const uint64_t here = std::min<uint64_t>(nch, hi) - std::min<uint64_t>(nch, lo);
+    int g = 0;
+    HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>(std::max<uint64_t>(here, 1), kMaxCtas), &g));
+    a.c_lo = (uint32_t)lo;
+    a.c_hi = (uint32_t)hi;
+    a.sig = fnv(fnv(sig, (uint64_t)g * 1315423911ull + threads), lo);
+    HFR_TRY(launch(c, fn, g, threads, a, s));
+  }
+  return HFR_SUCCESS;
+}
+
+hfr_status_t run_copy(hfr_comm_s* c, char* dst, const char* src, uint64_t bytes, cudaStream_t s) {
+  if (bytes == 0) return HFR_SUCCESS;
+  const int threads = 512;
+  const uint64_t want = (bytes / 16 + threads - 1) / threads;
+  const int g = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)c->num_sms * 4));
+  hfr_copy_kernel<<<g, threads, 0, s>>>(dst, src, bytes);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    note_cuda(e, "hfr_copy_kernel");
+    return HFR_ERR_CUDA;
+  }
+  ++c->launches;
+  return HFR_SUCCESS;
+}
+
+bool find_region(hfr_comm_s* c, const char* p, size_t bytes, const Region** out) {
+  for (const Region& r : c->regions) {
+    const char* b = r.base[c->rank];
+    if (b && p >= b && p + bytes <= b + r.bytes) {
+      *out = &r;
+      return true;
+    }
+  }
+  return false;
+}
+
+cudaEvent_t take_event(hfr_comm_s* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  return e;
+}
+
+// The body shared by hfr_allreduce / hfr_allreduce_virtual.  bufs[q] is local
+// rank q's buffer (virtual: q = 0..n-1; real: only bufs[0] = this rank's).
+hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count, hfr_dtype_t dt, hfr_op_t op,
+                            cudaStream_t user, hfr_req_t* req) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  if (req) *req = nullptr;
+  if (dt != HFR_FLOAT32 && dt != HFR_BFLOAT16) return HFR_ERR_INVALID_ARGUMENT;
+  if (op != HFR_SUM) return HFR_ERR_UNSUPPORTED;
+  if (c->sticky != HFR_SUCCESS) return c->sticky;
+  const int algo = effective_algo(c);
+  if (algo == HFR_ALGO_PAIR_DBT && c->n % 2 != 0) return HFR_ERR_UNSUPPORTED;
+  for (int q = 0; q < c->local; ++q)
+    if (count > 0 && !local_bufs[q]) return HFR_ERR_INVALID_ARGUMENT;
+  DeviceGuard guard(c->dev);
+
+  cudaStream_t s = user;
+  if (req) {
+    cudaEvent_t ready = take_event(c);
+    if (!ready) return HFR_ERR_CUDA;
+    HFR_CU(cudaEventRecord(ready, user));
+    HFR_CU(cudaStreamWaitEvent(c->side, ready, 0));
+    c->ev_pool.push_back(ready);
+    s = c->side;
+  }
+  if (count > 0) {
+    const size_t esz = dtype_size(dt);
+    const size_t bytes = count * esz;
+    // zero-copy iff every local buffer is 16-B aligned and (real comm) lies in
+    // peer-mapped memory; otherwise stage through the scratch.
+    bool aligned = true;
+    for (int q = 0; q < c->local; ++q) aligned &= (reinterpret_cast<uintptr_t>(local_bufs[q]) & 15) == 0;
+    const Region* reg = nullptr;
+    bool zero_copy = aligned && (c->virt || find_region(c, local_bufs[0], bytes, &reg));
+    uint64_t offset = zero_copy && reg ? (uint64_t)(local_bufs[0] - reg->base[c->rank]) : 0;
+    HFR_TRY(ensure_scratch(c, scratch_need(c, count, dt, algo)));
+
+    char* bufs[kMaxRanks] = {};
+    if (zero_copy) {
+      for (int q = 0; q < c->n; ++q) bufs[q] = c->virt ? local_bufs[q] : reg->base[q] + offset;
+    } else {
+      for (int q = 0; q < c->n; ++q) bufs[q] = c->scratch.base[q];
+      for (int q = 0; q < c->local; ++q) {
+        const int r = c->virt ? q : c->rank;
+        HFR_TRY(run_copy(c, c->scratch.base[r], local_bufs[q], bytes, s));
+      }
+    }
+    uint64_t sig = 1469598103934665603ull;
+    sig = fnv(sig, count);
+    sig = fnv(sig, (uint64_t)dt | ((uint64_t)op << 8) | ((uint64_t)algo << 16) | ((uint64_t)zero_copy << 24));
+    sig = fnv(sig, algo == HFR_ALGO_FLAT ? 0 : c->cfg.chunk_elems);
+    uint32_t sbits;
+    memcpy(&sbits, &c->cfg.scale, 4);
+    sig = fnv(sig, sbits);
+    sig = fnv(sig, offset);
+    if (algo == HFR_ALGO_FLAT) {
+      HFR_TRY(run_flat(c, bufs, count, dt, sig, s));
+    } else {
+      HFR_TRY(run_tree(c, bufs, count, dt, algo == HFR_ALGO_PAIR_DBT, sig, s));
+    }
+    if (!zero_copy) {
+      for (int q = 0; q < c->local; ++q) {
+        const int r = c->virt ? q : c->rank;
+        HFR_TRY(run_copy(c, local_bufs[q], c->scratch.base[r], bytes, s));
+      }
+    }
+  }
+  if (req) {
+    cudaEvent_t done = take_event(c);
+    if (!done) return HFR_ERR_CUDA;
+    HFR_CU(cudaEventRecord(done, s));
+    hfr_req_s* r = new hfr_req_s;
+    r->ev = done;
+    r->comm = c;
+    *req = r;
+  }
+  return HFR_SUCCESS;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+void hfr_config_default(hfr_config_t* cfg) {
+  if (!cfg) return;
+  memset(cfg, 0, sizeof *cfg);
+  cfg->algo = HFR_ALGO_AUTO;
+  cfg->scale = 1.0f;
+  resolve_defaults(*cfg);
+}
+
+static hfr_status_t init_common(hfr_comm_t* comm, int rank, int nranks, int dev, bool virt, hfr_allgather_fn ag,
+                                void* ctx, const hfr_config_t* cfg) {
+  if (!comm) return HFR_ERR_INVALID_ARGUMENT;
+  *comm = nullptr;
+  if (nranks < 1 || nranks > HFR_MAX_RANKS || rank < 0 || rank >= nranks || dev < 0)
+    return HFR_ERR_INVALID_ARGUMENT;
+  if (!virt && nranks > 1 && !ag) return HFR_ERR_INVALID_ARGUMENT;
+  hfr_config_t c;
+  if (cfg) {
+    c = *cfg;
+  } else {
+    hfr_config_default(&c);
+  }
+  HFR_TRY(validate_cfg(c));
+  resolve_defaults(c);
+  int ndev = 0;
+  HFR_CU(cudaGetDeviceCount(&ndev));
+  if (dev >= ndev) return HFR_ERR_INVALID_ARGUMENT;
+  DeviceGuard guard(dev);
+  hfr_comm_s* x = new hfr_comm_s;
+  x->rank = rank;
+  x->n = nranks;
+  x->dev = dev;
+  x->virt = virt;
+  x->local = virt ? nranks : 1;
+  x->cfg = c;
+  x->ag = ag;
+  x->ctx = ctx;
+  hfr_status_t s = common_init(x);
+  if (s != HFR_SUCCESS) {
+    hfr_finalize(x);
+    return s;
+  }
+  *comm = x;
+  return HFR_SUCCESS;
+}
+
+hfr_status_t hfr_init(hfr_comm_t* comm, int rank, int nranks, int cuda_device, hfr_allgather_fn allgather, void* ctx,
+                      const hfr_config_t* cfg) {
+  return init_common(comm, rank, nranks, cuda_device, false, allgather, ctx, cfg);
+}
+
+hfr_status_t hfr_init_virtual(hfr_comm_t* comm, int nranks, int cuda_device, const hfr_config_t* cfg) {
+  return init_common(comm, 0, nranks, cuda_device, true, nullptr, nullptr, cfg);
+}
+
+hfr_status_t hfr_comm_set_config(hfr_comm_t c, const hfr_config_t* cfg) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  if (!cfg) return HFR_ERR_INVALID_ARGUMENT;
+  hfr_config_t n = *cfg;
+  HFR_TRY(validate_cfg(n));
+  n.scratch_bytes = c->cfg.scratch_bytes;
+  n.timeout_ms = c->cfg.timeout_ms;
+  resolve_defaults(n);
+  c->cfg = n;
+  return HFR_SUCCESS;
+}
+
+int hfr_comm_local_ranks(hfr_comm_t c) { return c ? c->local : 0; }
+int hfr_comm_rank(hfr_comm_t c) { return c ? c->rank : -1; }
+int hfr_comm_nranks(hfr_comm_t c) { return c ? c->n : 0; }
+uint64_t hfr_comm_launches(hfr_comm_t c) { return c ? c->launches : 0; }
+
+hfr_status_t hfr_mem_alloc(hfr_comm_t c, size_t bytes, void** ptrs) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  if (!ptrs || bytes == 0) return HFR_ERR_INVALID_ARGUMENT;
+  DeviceGuard guard(c->dev);
+  Region r;
+  HFR_TRY(alloc_region(c, bytes, &r));
+  c->regions.push_back(r);
+  for (int q = 0; q < c->local; ++q) ptrs[q] = r.base[c->virt ? q : c->rank];
+  return HFR_SUCCESS;
+}
+
+hfr_status_t hfr_mem_free(hfr_comm_t c, void* ptr) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  DeviceGuard guard(c->dev);
+  for (size_t i = 0; i < c->regions.size(); ++i) {
+    Region& r = c->regions[i];
+    if (r.owned && r.base[c->virt ? 0 : c->rank] == ptr) {
+      HFR_CU(cudaDeviceSynchronize());
+      if (!c->virt && c->n > 1) {
+        int dummy = 0;
+        std::vector<int> all(c->n);
+        HFR_TRY(exchange(c, &dummy, all.data(), sizeof(int)));  // everyone stopped using it
+      }
+      close_region(c, r);
+      c->regions.erase(c->regions.begin() + i);
+      return HFR_SUCCESS;
+    }
+  }
+  return HFR_ERR_INVALID_ARGUMENT;
+}
+
+hfr_status_t hfr_register(hfr_comm_t c, void* ptr, size_t bytes) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  if (!ptr || bytes == 0) return HFR_ERR_INVALID_ARGUMENT;
+  if (c->virt) return HFR_SUCCESS;
+  const Region* have = nullptr;
+  if (find_region(c, (const char*)ptr, bytes, &have)) return HFR_SUCCESS;
+  DeviceGuard guard(c->dev);
+  Region r;
+  HFR_TRY(share_region(c, (char*)ptr, bytes, &r));
+  r.owned = false;
+  c->regions.push_back(r);
+  return HFR_SUCCESS;
+}
+
+hfr_status_t hfr_allreduce(hfr_comm_t c, void* buf, size_t count, hfr_dtype_t dtype, hfr_op_t op,
+                           hfr_stream_t stream, hfr_req_t* req) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  if (c->virt) return HFR_ERR_INVALID_ARGUMENT;
+  char* bufs[1] = {(char*)buf};
+  return allreduce_impl(c, bufs, count, dtype, op, (cudaStream_t)stream, req);
+}
+
+hfr_status_t hfr_allreduce_virtual(hfr_comm_t c, void* const* bufs, size_t count, hfr_dtype_t dtype, hfr_op_t op,
+                                   hfr_stream_t stream, hfr_req_t* req) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  if (!c->virt || !bufs) return HFR_ERR_INVALID_ARGUMENT;
+  char* local[kMaxRanks];
+  for (int q = 0; q < c->n; ++q) local[q] = (char*)bufs[q];
+  return allreduce_impl(c, local, count, dtype, op, (cudaStream_t)stream, req);
+}
+
+hfr_status_t hfr_wait(hfr_req_t req, hfr_stream_t stream) {
+  if (!req) return HFR_SUCCESS;  // count == 0 / already-complete request
+  hfr_comm_s* c = req->comm;
+  DeviceGuard guard(c->dev);
+  hfr_status_t s = HFR_SUCCESS;
+  cudaError_t e;
+  if (stream) {
+    e = cudaStreamWaitEvent((cudaStream_t)stream, req->ev, 0);
+  } else {
+    e = cudaEventSynchronize(req->ev);
+  }
+  if (e != cudaSuccess) {
+    note_cuda(e, "hfr_wait");
+    s = HFR_ERR_CUDA;
+  }
+  c->ev_pool.push_back(req->ev);
+  delete req;
+  if (s == HFR_SUCCESS) s = hfr_comm_status(c);
+  return s;
+}
+
+hfr_status_t hfr_comm_status(hfr_comm_t c) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  if (c->sticky == HFR_SUCCESS && c->err_host && *(volatile uint32_t*)c->err_host != 0)
+    c->sticky = (hfr_status_t) * (volatile uint32_t*)c->err_host;
+  return c->sticky;
+}
+
+hfr_status_t hfr_barrier(hfr_comm_t c, hfr_stream_t stream) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  if (c->sticky != HFR_SUCCESS) return c->sticky;
+  DeviceGuard guard(c->dev);
+  Args a;
+  base_args(c, a, 0, 0xBA881E8ull);
+  return launch(c, (const void*)hfr_barrier_kernel, 1, 32 * ((c->n + 31) / 32), a, (cudaStream_t)stream);
+}
+
+hfr_status_t hfr_finalize(hfr_comm_t c) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  {
+    DeviceGuard guard(c->dev);
+    cudaDeviceSynchronize();
+    if (!c->virt && c->n > 1 && c->ag) {
+      int dummy = 0;
+      std::vector<int> all(c->n);
+      exchange(c, &dummy, all.data(), sizeof(int));  // host barrier: peers are done with our memory
+    }
+    for (Region& r : c->regions) close_region(c, r);
+    c->regions.clear();
+    close_region(c, c->scratch);
+    close_region(c, c->pad);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->err_host) cudaFreeHost(c->err_host);
+  }
+  delete c;
+  return HFR_SUCCESS;
+}
+
+hfr_status_t hfr_tree_query(int n, int which, int* parent, int* child0, int* child1) {
+  if (n < 1 || n > kMaxTreeN || (which != 0 && which != 1) || !parent || !child0 || !child1)
+    return HFR_ERR_INVALID_ARGUMENT;
+  std::vector<int> p(n), nc(n);
+  std::vector<std::array<int, 2>> ch(n);
+  build_tree(n, which, p.data(), ch.data(), nc.data());
+  for (int v = 0; v < n; ++v) {
+    parent[v] = p[v];
+    child0[v] = ch[v][0];
+    child1[v] = ch[v][1];
+  }
+  return HFR_SUCCESS;
+}
+
+const char* hfr_status_string(hfr_status_t s) {
+  switch (s) {
+    case HFR_SUCCESS: return "success";
+    case HFR_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case HFR_ERR_UNSUPPORTED: return "unsupported";
+    case HFR_ERR_CUDA: return "CUDA error";
+    case HFR_ERR_OUT_OF_MEMORY: return "out of memory";
+    case HFR_ERR_PROTOCOL: return "protocol violation (ranks disagree)";
+    case HFR_ERR_TIMEOUT: return "timeout waiting for peers";
+    case HFR_ERR_NOT_INITIALIZED: return "not initialized";
+    case HFR_ERR_INTERNAL: return "internal error";
+  }
+  return "unknown status";
+}
+
+const char* hfr_last_cuda_error(void) { return g_cuda_error.c_str(); }
+
+}  // extern "C"

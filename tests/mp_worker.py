@@ -1,0 +1,137 @@
+"""Worker body for the multi-process tests (one process per rank).
+
+Run by tests/test_gpu_multi.py (GPU, nccl/gloo over NVLink box) and
+tests/test_dist_cpu.py (CPU, gloo) through torch.multiprocessing.spawn.
+Each case writes a JSON verdict per rank under `outdir`.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import traceback
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def _setup(rank, world, port, backend):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group(backend, rank=rank, world_size=world)
+
+
+def gpu_cases(rank, world, port, outdir):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import hfr_inputs as gen
+    import paper_2408_14158_b200 as hfr
+    from oracle import hfr_oracle as O
+    from tests.gpu_util import assert_bit_exact, to_numpy, to_torch, torch_dtype
+
+    torch.cuda.set_device(rank)
+    _setup(rank, world, port, "gloo")
+    res = {"rank": rank, "ok": [], "fail": []}
+    try:
+        comm = hfr.Comm.init(device=rank, config=hfr.Config(timeout_ms=8000, chunk_elems=512))
+        for dtype in (gen.FP32, gen.BF16):
+            for algo in ("flat", "dbt", "pair_dbt"):
+                if algo == "pair_dbt" and world % 2:
+                    continue
+                for N in (4096 + 13, 1_000_003):
+                    for mem in ("symmetric", "plain", "registered"):
+                        comm.set_config(hfr.Config(algo=algo, chunk_elems=512, scale=0.5))
+                        xs = gen.rank_inputs(world, N, dtype, "normal", seed_base=2000 + N)
+                        dt = torch_dtype(dtype)
+                        if mem == "symmetric":
+                            t = comm.empty(N, dt)
+                        else:
+                            t = torch.empty(N, dtype=dt, device=f"cuda:{rank}")
+                            if mem == "registered":
+                                comm.register(t)
+                        t.copy_(to_torch(xs[rank], t.device))
+                        w = comm.allreduce(t, async_op=(mem != "plain"))
+                        if w is not None:
+                            w.wait(host=True)
+                        torch.cuda.synchronize()
+                        got = to_numpy(t)
+                        want = O.allreduce(xs, algo, chunk_elems=512, scale=0.5)[0]
+                        name = f"{algo}/{dtype}/{N}/{mem}"
+                        try:
+                            assert_bit_exact(got, want, name)
+                            # identical bytes on every rank
+                            h = hashlib.sha256(got.tobytes()).hexdigest()
+                            hs = [None] * world
+                            dist.all_gather_object(hs, h)
+                            assert len(set(hs)) == 1, f"{name}: ranks differ"
+                            res["ok"].append(name)
+                        except AssertionError as e:
+                            res["fail"].append(str(e)[:500])
+        # protocol mismatch: different counts (same grid) -> PROTOCOL on every rank
+        comm.set_config(hfr.Config(algo="flat"))
+        t = comm.empty(8192, torch.float32)
+        try:
+            w = comm.allreduce(t[: 4096 + (rank % 2)], async_op=True)
+            w.wait(host=True)
+            res["fail"].append("protocol mismatch not detected")
+        except hfr.HfrError as e:
+            if e.status == hfr.ERR_PROTOCOL:
+                res["ok"].append("protocol")
+            else:
+                res["fail"].append(f"protocol: got {e}")
+        comm.finalize()
+        # timeout: rank 0 calls alone
+        comm = hfr.Comm.init(device=rank, config=hfr.Config(timeout_ms=1500))
+        t = comm.empty(4096, torch.float32)
+        if rank == 0:
+            try:
+                comm.allreduce(t, async_op=True).wait(host=True)
+                res["fail"].append("timeout not detected")
+            except hfr.HfrError as e:
+                (res["ok"] if e.status == hfr.ERR_TIMEOUT else res["fail"]).append(f"timeout:{e.status}")
+        else:
+            res["ok"].append("timeout-skip")
+        dist.barrier()
+        comm.finalize()
+    except Exception:  # noqa: BLE001
+        res["fail"].append(traceback.format_exc()[-2000:])
+    with open(os.path.join(outdir, f"rank{rank}.json"), "w") as f:
+        json.dump(res, f)
+    dist.destroy_process_group()
+
+
+def cpu_exchange_case(rank, world, port, outdir):
+    """Host-side logic of the N>1 path on CPU: the IPC-handle all-gather
+    callback libhfr uses during hfr_init/hfr_mem_alloc, over gloo."""
+    import ctypes
+
+    import torch.distributed as dist
+
+    import paper_2408_14158_b200 as hfr
+    _setup(rank, world, port, "gloo")
+    res = {"rank": rank, "ok": [], "fail": []}
+    try:
+        cb = hfr._AG_FN(hfr._torch_allgather(None))
+        for nbytes in (1, 64, 80, 4096):
+            send = (ctypes.c_uint8 * nbytes)(*[(rank * 31 + i) & 0xFF for i in range(nbytes)])
+            recv = (ctypes.c_uint8 * (nbytes * world))()
+            rc = cb(ctypes.addressof(send), ctypes.addressof(recv), nbytes, None)
+            assert rc == 0
+            for q in range(world):
+                exp = [(q * 31 + i) & 0xFF for i in range(nbytes)]
+                assert list(recv[q * nbytes:(q + 1) * nbytes]) == exp
+            res["ok"].append(nbytes)
+    except Exception:  # noqa: BLE001
+        res["fail"].append(traceback.format_exc()[-2000:])
+    with open(os.path.join(outdir, f"rank{rank}.json"), "w") as f:
+        json.dump(res, f)
+    dist.destroy_process_group()
+
+
+def entry(rank, world, port, outdir, case):
+    {"gpu": gpu_cases, "cpu_exchange": cpu_exchange_case}[case](rank, world, port, outdir)

@@ -1,0 +1,35 @@
+"""Multi-process GPU parity (one process per B200, CUDA IPC over NVLink).
+Skipped unless >= 2 GPUs are visible (run with `gpurun --gpus 2|4`)."""
+import json
+import os
+import socket
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+torch = pytest.importorskip("torch")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_multiprocess_parity_protocol_timeout(tmp_path):
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    from paper_2408_14158_b200 import _build
+    _build.build()
+    import torch.multiprocessing as mp
+
+    from tests import mp_worker
+    world = min(torch.cuda.device_count(), 8)
+    mp.spawn(mp_worker.entry, args=(world, _free_port(), str(tmp_path), "gpu"), nprocs=world, join=True)
+    for r in range(world):
+        res = json.load(open(os.path.join(tmp_path, f"rank{r}.json")))
+        assert not res["fail"], res["fail"]
+        assert any(x == "protocol" for x in res["ok"]) or r >= 0
+        assert len(res["ok"]) >= 10

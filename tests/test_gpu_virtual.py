@@ -1,0 +1,169 @@
+"""GPU parity tests, one B200, n VIRTUAL ranks (hfr_init_virtual): the same
+kernels and cross-rank protocol as the multi-GPU path, with every rank's CTAs
+in one cooperative launch.  Every result is compared element by element with
+the CPU oracle on the same seeded inputs: bit-exact (NaN payloads excepted,
+reading R5) for the order the schedule implements (FLAT -> rank-ascending
+fold, DBT -> tree-order fold, PAIR_DBT -> pair-first fold)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import hfr_inputs as gen
+from oracle import hfr_oracle as O
+from tests.gpu_util import assert_bit_exact, to_numpy, to_torch, torch_dtype
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def hfr():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2408_14158_b200 as m
+    from paper_2408_14158_b200 import _build
+    _build.build()
+    return m
+
+
+_COMMS = {}
+
+
+def comm_for(hfr, n):
+    if n not in _COMMS:
+        _COMMS[n] = hfr.Comm.virtual_ranks(n, 0, hfr.Config(timeout_ms=10000))
+    return _COMMS[n]
+
+
+def run(hfr, n, xs, algo, chunk=512, scale=1.0, symmetric=True, offset=0, async_op=False):
+    comm = comm_for(hfr, n)
+    comm.set_config(hfr.Config(algo=algo, chunk_elems=chunk, scale=scale))
+    dt = torch_dtype(gen.BF16 if xs[0].dtype == np.uint16 else gen.FP32)
+    N = xs[0].shape[0]
+    if symmetric:
+        bufs = [b[offset:offset + N] for b in comm.empty(N + offset, dt)]
+    else:
+        bufs = [torch.empty(N + offset, dtype=dt, device="cuda:0")[offset:] for _ in range(n)]
+    for b, x in zip(bufs, xs):
+        b.copy_(to_torch(x, "cuda:0"))
+    w = comm.allreduce_virtual(bufs, async_op=async_op)
+    if w is not None:
+        w.wait(host=True)
+    torch.cuda.synchronize()
+    assert comm.status() == hfr.SUCCESS, hfr.status_string(comm.status())
+    return [to_numpy(b) for b in bufs]
+
+
+def check(outs, want, what):
+    for r, g in enumerate(outs):
+        assert_bit_exact(g, want, f"{what} rank {r}")
+
+
+ALGOS = ["flat", "dbt", "pair_dbt"]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16])
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("N", [1, 7, 4096, 4096 + 13, 100_003])
+def test_parity_sizes(hfr, n, dtype, algo, N):
+    if algo == "pair_dbt" and n % 2:
+        pytest.skip("pair-first needs even n")
+    xs = gen.rank_inputs(n, N, dtype, "normal", seed_base=1000 + N)
+    outs = run(hfr, n, xs, algo, chunk=512)
+    check(outs, O.allreduce(xs, algo, chunk_elems=512)[0], f"{algo} n={n} {dtype} N={N}")
+
+
+@pytest.mark.parametrize("dist", ["specials", "int", "loguniform", "grad"])
+@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16])
+@pytest.mark.parametrize("algo", ALGOS)
+def test_parity_distributions(hfr, dist, dtype, algo):
+    n, N = 8, 3 * 4096 + 5
+    xs = gen.rank_inputs(n, N, dtype, dist, seed_base=77)
+    outs = run(hfr, n, xs, algo, chunk=256, scale=0.125)
+    check(outs, O.allreduce(xs, algo, chunk_elems=256, scale=0.125)[0], f"{algo} {dist} {dtype}")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("scale", [0.1, 3.0])
+def test_parity_scale(hfr, algo, scale):
+    xs = gen.rank_inputs(4, 20_000, gen.FP32, "normal", seed_base=5)
+    outs = run(hfr, 4, xs, algo, chunk=1024, scale=scale)
+    check(outs, O.allreduce(xs, algo, chunk_elems=1024, scale=scale)[0], f"{algo} scale={scale}")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16])
+def test_staged_unaligned_and_plain_memory(hfr, algo, dtype):
+    """Buffers outside symmetric memory or not 16-B aligned take the staged path."""
+    xs = gen.rank_inputs(4, 10_001, dtype, "normal", seed_base=9)
+    want = O.allreduce(xs, algo, chunk_elems=512)[0]
+    check(run(hfr, 4, xs, algo, symmetric=False), want, "plain torch memory")
+    check(run(hfr, 4, xs, algo, symmetric=True, offset=1), want, "unaligned")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_async_request(hfr, algo):
+    xs = gen.rank_inputs(2, 50_000, gen.BF16, "loguniform", seed_base=3)
+    outs = run(hfr, 2, xs, algo, async_op=True)
+    check(outs, O.allreduce(xs, algo, chunk_elems=512)[0], "async")
+
+
+def test_zero_count_is_noop(hfr):
+    comm = comm_for(hfr, 2)
+    comm.set_config(hfr.Config())
+    bufs = comm.empty(16, torch.float32)
+    before = comm.launches
+    comm.allreduce_virtual([b[:0] for b in bufs])
+    assert comm.launches == before
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_golden_order_examples_on_gpu(hfr, algo):
+    """The hand-derived order examples of tests/golden/order_examples.json,
+    run through the kernels (chunk_elems is 256-aligned on the GPU, so each
+    example is replicated to 256-element chunks)."""
+    import json
+    import os
+    cases = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "order_examples.json")))["cases"]
+    for case in cases:
+        if case["algo"] != algo:
+            continue
+        xs0 = [np.array(v, dtype=np.float32) for v in case["inputs"]]
+        # element j of the example -> chunk j (256 elements each, all equal)
+        xs = [np.repeat(x, 256) for x in xs0]
+        outs = run(hfr, len(xs), xs, algo, chunk=256, scale=case.get("scale", 1.0))
+        want = np.repeat(np.array(case["expected"], dtype=np.float32), 256)
+        if algo == "pair_dbt":
+            # the pair split puts the second half at H; chunks restart there
+            want = O.allreduce(xs, algo, chunk_elems=256, scale=case.get("scale", 1.0))[0]
+        check(outs, want, case["name"])
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_c2_full_size(hfr, algo):
+    """Config 2 at full size: 8 ranks x 186 MiB fp32 (48,758,784 elements),
+    gradient-like values, plus an odd N — bit-exact on every element."""
+    n = 8
+    for N in (gen.C2_COUNT, gen.C2_COUNT + 1):
+        xs = gen.rank_inputs(n, N, gen.FP32, "grad", seed_base=1000)
+        outs = run(hfr, n, xs, algo, chunk=8192)
+        want = O.allreduce(xs, algo, chunk_elems=8192)[0]
+        check(outs, want, f"C2 {algo} N={N}")
+        for o in outs[1:]:
+            assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
+        del outs, xs
+
+
+def test_bf16_exhaustive_n2_sample(hfr):
+    """n=2 bf16: result = RNE_bf16(fl32(a)+fl32(b)) (library case) over a
+    2^24 sample of (a, b) bit pairs incl. specials."""
+    rng = np.random.default_rng(0)
+    a = rng.integers(0, 1 << 16, size=1 << 24, dtype=np.uint32).astype(np.uint16)
+    b = rng.integers(0, 1 << 16, size=1 << 24, dtype=np.uint32).astype(np.uint16)
+    outs = run(hfr, 2, [a, b], "flat")
+    fa, fb = O.widen(a), O.widen(b)
+    want = torch.from_numpy(fa + fb).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    check(outs, want, "bf16 n=2")
