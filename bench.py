@@ -271,18 +271,20 @@ def main():
         launches = comm.launches - l0
         return max_over_ranks(e0.elapsed_time(e1) / 1e3 / steps), launches
 
-    # warm-up, then a clock soak (untimed) with the sampler on, then the timed region
+    # warm-up; the clock sampler runs over the timed region and an untimed soak
+    # right after it (so it collects samples even when K steps take ~10 ms)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     clocks = Clocks(local)
     clocks.start()
+    time.sleep(0.15)
+    t_step, launches = timed(step, args.steps)
     t_soak = time.perf_counter() + args.soak
     while time.perf_counter() < t_soak:
         for _ in range(10):
             step()
         torch.cuda.synchronize()
-    t_step, launches = timed(step, args.steps)
     ck = clocks.stop()
     if comm.status() != hfr.SUCCESS:
         raise SystemExit(f"hfr error: {hfr.status_string(comm.status())}")
