@@ -292,8 +292,14 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
     const uint64_t lo = nvec * rank / n, hi = nvec * (rank + 1) / n;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     if constexpr (NR > 0) {
-      for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += U * stride)
-        flat_vecs<E, NR, U>(a, i, stride, hi);
+      // warp tiles of U*32 consecutive vectors (U*512 B contiguous per rank
+      // buffer): lane l of the warp owning tile t handles vectors
+      // t*U*32 + u*32 + l, u < U.  Tiles are dealt round-robin to all warps.
+      const uint64_t lane = threadIdx.x & 31;
+      const uint64_t warps = stride / 32;
+      const uint64_t w = ((uint64_t)b * blockDim.x + threadIdx.x) / 32;
+      for (uint64_t t0 = lo + w * (U * 32); t0 < hi; t0 += warps * (U * 32))
+        flat_vecs<E, NR, U>(a, t0 + lane, 32, hi);
     } else {
       for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += stride)
         flat_vec_dyn<E>(a, n, i);

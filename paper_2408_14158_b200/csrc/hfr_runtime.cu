@@ -492,8 +492,12 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   for (uint64_t lo = 0; lo < std::max<uint64_t>(nch, 1); lo += kMaxChunks) {
     const uint64_t hi = lo + kMaxChunks;
     const uint64_t here = std::min<uint64_t>(nch, hi) - std::min<uint64_t>(nch, lo);
+    // An EVEN number of CTAs per rank: CTA b then only ever sees chunks of
+    // tree b & 1, so the two trees' dependency chains never interleave inside
+    // one CTA (a rank is the root of one tree and a leaf of the other).
     int g = 0;
-    HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>(std::max<uint64_t>(here, 1), kMaxCtas), &g));
+    HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>(std::max<uint64_t>(here, 2), kMaxCtas), &g));
+    g = std::max(2, g & ~1);
     a.c_lo = (uint32_t)lo;
     a.c_hi = (uint32_t)hi;
     a.sig = fnv(fnv(sig, (uint64_t)g * 1315423911ull + threads), lo);

@@ -1,0 +1,127 @@
+#!/usr/bin/env python
+"""Performance sweeps (not the bench contract): busBW of HFReduce schedules
+and NCCL over message sizes / chunk sizes / CTA counts.
+
+  python tools/sweep.py --virtual 8 ...                      (1 GPU)
+  torchrun --nproc-per-node N tools/sweep.py ...             (N GPUs)
+
+Prints one JSON line per measured point (rank 0).  Timing protocol as in
+bench.py: host + device barrier, CUDA events around `iters` back-to-back calls
+on the current stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import itertools
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--virtual", type=int, default=0)
+    p.add_argument("--sizes", default=str(186 << 20), help="comma list of bytes per rank")
+    p.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    p.add_argument("--algos", default="flat")
+    p.add_argument("--chunks", default="0")
+    p.add_argument("--ctas", default="0")
+    p.add_argument("--threads", default="0")
+    p.add_argument("--iters", type=int, default=0)
+    p.add_argument("--nccl", action="store_true")
+    p.add_argument("--out", default="")
+    a = p.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2408_14158_b200 as hfr
+    from paper_2408_14158_b200 import _build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    _build.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    multi = world > 1
+    if multi:
+        dist.init_process_group("nccl", device_id=dev)
+    n = world if multi else a.virtual
+    tdt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
+    esz = 2 if a.dtype == "bf16" else 4
+    sizes = [int(s) for s in a.sizes.split(",")]
+    comm = hfr.Comm.init(device=local) if multi else hfr.Comm.virtual_ranks(n, local)
+    big = max(sizes) // esz
+    bufs = comm.empty(big, tdt)
+    bufs = bufs if isinstance(bufs, list) else [bufs]
+    for b in bufs:
+        b.normal_()
+    stream = torch.cuda.current_stream()
+    out = open(a.out, "a") if (a.out and rank == 0) else None
+
+    def mx(v):
+        if not multi:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timeit(fn, iters):
+        for _ in range(3):
+            fn()
+        if multi:
+            dist.barrier()
+        comm.barrier(stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return mx(e0.elapsed_time(e1) / 1e3 / iters)
+
+    def emit(d):
+        if rank == 0:
+            s = json.dumps(d)
+            print(s, flush=True)
+            if out:
+                out.write(s + "\n")
+                out.flush()
+
+    for size in sizes:
+        cnt = size // esz
+        views = [b[:cnt] for b in bufs]
+        iters = a.iters or (200 if size <= (1 << 20) else 50 if size <= (64 << 20) else 20)
+        for algo, chunk, ctas, thr in itertools.product(a.algos.split(","), map(int, a.chunks.split(",")),
+                                                        map(int, a.ctas.split(",")), map(int, a.threads.split(","))):
+            if algo == "pair_dbt" and n % 2:
+                continue
+            comm.set_config(hfr.Config(algo=algo, chunk_elems=chunk, max_ctas=ctas, threads=thr,
+                                       scale=1.0 / n, timeout_ms=30000))
+            fn = (lambda: comm.allreduce(views[0])) if multi else (lambda: comm.allreduce_virtual(views))
+            t = timeit(fn, iters)
+            st = comm.status()
+            if st != hfr.SUCCESS:
+                raise SystemExit(f"hfr error {hfr.status_string(st)}")
+            emit({"impl": "hfr", "n": n, "virtual": not multi, "dtype": a.dtype, "bytes": size, "algo": algo,
+                  "chunk": chunk, "ctas": ctas, "threads": thr, "us": t * 1e6,
+                  "busbw": size / t * 2 * (n - 1) / n / 1e9, "algbw": size / t / 1e9})
+        if multi and a.nccl:
+            t_ = torch.empty(cnt, dtype=tdt, device=dev).normal_()
+            tn = timeit(lambda: dist.all_reduce(t_), iters)
+            emit({"impl": "nccl", "n": n, "dtype": a.dtype, "bytes": size, "us": tn * 1e6,
+                  "busbw": size / tn * 2 * (n - 1) / n / 1e9, "algbw": size / tn / 1e9,
+                  "env": {k: v for k, v in os.environ.items() if k.startswith("NCCL_")}})
+            del t_
+    comm.finalize()
+    if multi:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
