@@ -1,0 +1,121 @@
+"""HaiScale-style DDP gradient bucketing over HFReduce (§8 row a6).
+
+PAPER.md:449-453 (§5 "HaiScale DDP Overlap AllReduce in Training"): "During the
+backpropagation phase, HaiScale DDP performs an asynchronous allreduce
+operation on the computed gradients, allowing this communication to overlap
+with the computation involved in backpropagation."
+
+B200 recast: every gradient lives in ONE symmetric peer-mapped arena
+(hfr_mem_alloc) laid out in backward order, cut into fixed-size buckets
+(64 MiB by default, config 5).  As the backward pass finishes the last
+gradient touching a bucket, the bucket's hfr_allreduce is enqueued
+asynchronously: the comm side stream waits on an event recorded on the
+compute stream, so the reduction overlaps the rest of the backward.  finish()
+orders every bucket's completion back onto the compute stream before the
+optimizer step.  The comm kernels are capped at `max_ctas` CTAs so they leave
+most SMs to the backward GEMMs (unlike the paper's copy-engine HFReduce,
+PAPER.md:375, an SM-driven allreduce is not free — DESIGN.md §6).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Sequence, Tuple
+
+
+def plan_buckets(numels: Sequence[int], bucket_elems: int) -> Tuple[List[Tuple[int, int]], List[Tuple[int, int]],
+                                                                    List[List[int]]]:
+    """Lay parameters out back to back in the given (backward) order and cut
+    the arena into buckets of `bucket_elems` elements (the last one ragged).
+
+    Returns (param_ranges, bucket_ranges, bucket_params) where param_ranges[i]
+    = [start, end) of parameter i in the arena, bucket_ranges[k] = [start, end)
+    of bucket k, and bucket_params[k] = indices of the parameters overlapping
+    bucket k (a bucket is ready once all of them are written)."""
+    if bucket_elems <= 0:
+        raise ValueError("bucket_elems must be positive")
+    ranges = []
+    off = 0
+    for m in numels:
+        if m < 0:
+            raise ValueError("negative numel")
+        ranges.append((off, off + m))
+        off += m
+    total = off
+    buckets = [(s, min(s + bucket_elems, total)) for s in range(0, total, bucket_elems)]
+    members: List[List[int]] = [[] for _ in buckets]
+    for i, (s, e) in enumerate(ranges):
+        if e == s:
+            continue
+        for k in range(s // bucket_elems, (e - 1) // bucket_elems + 1):
+            members[k].append(i)
+    return ranges, buckets, members
+
+
+@dataclass
+class BucketStats:
+    launched: int = 0
+    bytes: int = 0
+
+
+class HaiScaleDDP:
+    """Gradient arena + asynchronous bucketed allreduce for one rank.
+
+    Usage per step:
+        ddp.zero_grad()                     (optional)
+        for i in backward order: write ddp.grad(i); ddp.mark_ready(i, stream)
+        ddp.finish(stream)                  (stream waits for every bucket)
+    """
+
+    def __init__(self, comm, numels: Sequence[int], dtype, bucket_bytes: int = 64 << 20):
+        import torch
+        self.comm = comm
+        self.dtype = dtype
+        esz = torch.tensor([], dtype=dtype).element_size()
+        self.bucket_elems = max(1, bucket_bytes // esz)
+        self.param_ranges, self.bucket_ranges, self.bucket_params = plan_buckets(list(numels), self.bucket_elems)
+        self.total = self.param_ranges[-1][1] if self.param_ranges else 0
+        self.arena = comm.empty(max(1, self.total), dtype)
+        if isinstance(self.arena, list):
+            raise ValueError("HaiScaleDDP needs a real (one rank per process) comm")
+        self._pending = [len(m) for m in self.bucket_params]
+        self._bucket_of_param: List[List[int]] = [[] for _ in numels]
+        for k, mem in enumerate(self.bucket_params):
+            for i in mem:
+                self._bucket_of_param[i].append(k)
+        self._works = []
+        self.stats = BucketStats()
+
+    def grad(self, i: int):
+        s, e = self.param_ranges[i]
+        return self.arena[s:e]
+
+    def bucket(self, k: int):
+        s, e = self.bucket_ranges[k]
+        return self.arena[s:e]
+
+    def reset(self):
+        self._pending = [len(m) for m in self.bucket_params]
+        self._works = []
+
+    def mark_ready(self, i: int, stream=None):
+        """Parameter i's gradient has been enqueued on `stream`; launch the
+        allreduce of every bucket that just became complete."""
+        for k in self._bucket_of_param[i]:
+            self._pending[k] -= 1
+            if self._pending[k] == 0:
+                self._launch(k, stream)
+
+    def _launch(self, k: int, stream):
+        b = self.bucket(k)
+        self._works.append(self.comm.allreduce(b, async_op=True, stream=stream))
+        self.stats.launched += 1
+        self.stats.bytes += b.numel() * b.element_size()
+
+    def finish(self, stream=None):
+        """Make `stream` wait for every launched bucket (no host block)."""
+        for w in self._works:
+            w.wait(stream=stream)
+        self._works = []
+        if any(p != 0 for p in self._pending):
+            raise RuntimeError("finish() before every gradient was marked ready")
+        self.reset()

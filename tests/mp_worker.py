@@ -72,6 +72,24 @@ def gpu_cases(rank, world, port, outdir):
                             res["ok"].append(name)
                         except AssertionError as e:
                             res["fail"].append(str(e)[:500])
+        # HaiScale DDP: bucketed async allreduce == fold of the arena
+        from paper_2408_14158_b200.ddp import HaiScaleDDP
+        comm.set_config(hfr.Config(algo="flat", scale=0.5))
+        numels = [1000, 70000, 3, 250000, 4097]
+        ddp = HaiScaleDDP(comm, numels, torch.bfloat16, bucket_bytes=64 << 10)
+        stream = torch.cuda.current_stream()
+        xs_all = [gen.rank_input(r, ddp.total, gen.BF16, "normal", seed_base=4000) for r in range(world)]
+        for i, (s, e) in enumerate(ddp.param_ranges):
+            ddp.grad(i).copy_(to_torch(xs_all[rank][s:e], ddp.arena.device))
+            ddp.mark_ready(i, stream)
+        ddp.finish(stream)
+        torch.cuda.synchronize()
+        try:
+            assert ddp.stats.launched == len(ddp.bucket_ranges)
+            assert_bit_exact(to_numpy(ddp.arena[:ddp.total]), O.fold_ascending(xs_all, 0.5), "ddp")
+            res["ok"].append("ddp")
+        except AssertionError as e:
+            res["fail"].append(str(e)[:500])
         # protocol mismatch: different counts (same grid) -> PROTOCOL on every rank
         comm.set_config(hfr.Config(algo="flat"))
         t = comm.empty(8192, torch.float32)

@@ -1,0 +1,50 @@
+"""CPU tests of the HaiScale-DDP bucket planner (§8 a6)."""
+import pytest
+
+from paper_2408_14158_b200.ddp import plan_buckets
+
+
+def test_plan_tiles_exactly():
+    numels = [10, 0, 7, 33, 1, 64]
+    ranges, buckets, members = plan_buckets(numels, 16)
+    assert ranges[0] == (0, 10) and ranges[-1] == (51, 115)
+    assert buckets[0] == (0, 16) and buckets[-1] == (112, 115)
+    covered = []
+    for s, e in buckets:
+        covered.extend(range(s, e))
+    assert covered == list(range(115))
+    # every member overlaps its bucket; every overlapping param is a member
+    for k, (s, e) in enumerate(buckets):
+        want = [i for i, (a, b) in enumerate(ranges) if b > a and a < e and b > s]
+        assert members[k] == want
+
+
+@pytest.mark.parametrize("bucket", [1, 3, 64, 1000])
+def test_ready_order_launches_each_bucket_once(bucket):
+    numels = [5, 17, 3, 100, 2, 40]
+    _, buckets, members = plan_buckets(numels, bucket)
+    pending = [len(m) for m in members]
+    launched = []
+    for i in range(len(numels)):
+        for k, mem in enumerate(members):
+            if i in mem:
+                pending[k] -= 1
+                if pending[k] == 0:
+                    launched.append(k)
+    assert sorted(launched) == list(range(len(buckets)))
+    assert launched == sorted(launched)  # backward order fills buckets in order
+
+
+def test_c5_bucket_count():
+    """config 5: 7.0e9 bf16 = 14.0e9 B -> 208 x 64 MiB + one 41,356,288 B bucket."""
+    import tools.ddp_overlap as d
+    numels = [o * i for _, o, i in d.llama7b_layout()]
+    assert sum(numels) == 7_000_000_000
+    _, buckets, _ = plan_buckets(numels, (64 << 20) // 2)
+    assert len(buckets) == 209
+    assert (buckets[-1][1] - buckets[-1][0]) * 2 == 41_356_288
+
+
+def test_bad_bucket():
+    with pytest.raises(ValueError):
+        plan_buckets([1], 0)
