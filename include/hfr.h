@@ -58,12 +58,21 @@ typedef enum {
  *            of all n buffers over NVLink, folds in rank order 0..n-1 (fp32),
  *            scales, casts, and stores the result into all n buffers.  Result =
  *            rank-ascending fold (Algorithm 1 order).
+ *   ONESHOT  small messages: every rank pushes its whole buffer into every
+ *            peer's inbox, then folds all n copies locally in rank order.  Same
+ *            result bits as FLAT; one cross-rank handoff instead of two.
  *   DBT      the paper's double binary tree (Algorithm 2) as
  *            a push-only P2P schedule over the GPUs; chunk c rides tree c mod 2.
  *   PAIR_DBT "HFReduce with NVLink": pair (2k,2k+1) reduce,
  *            tree over the n/2 pair partials per half, pair all-gather.
- *   AUTO     = FLAT. */
-typedef enum { HFR_ALGO_AUTO = 0, HFR_ALGO_FLAT = 1, HFR_ALGO_DBT = 2, HFR_ALGO_PAIR_DBT = 3 } hfr_algo_t;
+ *   AUTO     ONESHOT up to oneshot_max_bytes, FLAT above. */
+typedef enum {
+    HFR_ALGO_AUTO = 0,
+    HFR_ALGO_FLAT = 1,
+    HFR_ALGO_DBT = 2,
+    HFR_ALGO_PAIR_DBT = 3,
+    HFR_ALGO_ONESHOT = 4
+} hfr_algo_t;
 
 /* All-gather callback used ONLY by the collective setup calls (hfr_init,
  * hfr_mem_alloc, hfr_register, hfr_finalize) to exchange CUDA IPC handles:
@@ -81,6 +90,8 @@ typedef struct {
     float scale;          /* gradient scale, multiplies the fp32 total once (reading R3); 1.0 = sum */
     size_t scratch_bytes; /* per-rank library scratch (staging + tree partials); 0 -> 256 MiB */
     int timeout_ms;       /* cross-rank spin-wait timeout; 0 -> 60000 */
+    size_t oneshot_max_bytes; /* largest message for ONESHOT (and AUTO's switch point); fixed at
+                                 init (sizes the per-rank inbox: 2 * nranks * this); 0 -> 512 KiB */
 } hfr_config_t;
 
 /* Fill *cfg with the defaults above (algo AUTO, scale 1.0). */
@@ -103,7 +114,8 @@ hfr_status_t hfr_init(hfr_comm_t* comm, int rank, int nranks, int cuda_device,
 hfr_status_t hfr_init_virtual(hfr_comm_t* comm, int nranks, int cuda_device, const hfr_config_t* cfg);
 
 /* COLLECTIVE.  Change algo / scale / chunk_elems / max_ctas / threads for
- * subsequent calls (scratch_bytes and timeout_ms are fixed at init). */
+ * subsequent calls (scratch_bytes, timeout_ms and oneshot_max_bytes are fixed
+ * at init). */
 hfr_status_t hfr_comm_set_config(hfr_comm_t comm, const hfr_config_t* cfg);
 
 /* Number of ranks this process drives: 1 for hfr_init comms, nranks for
@@ -136,7 +148,8 @@ hfr_status_t hfr_register(hfr_comm_t comm, void* ptr, size_t bytes);
  *   scale, cast to dtype.  Buffers outside hfr_mem_alloc / hfr_register memory
  *   or not 16-byte aligned are staged through the scratch (correct, slower).
  *   Ownership: caller owns buf; it must stay allocated and untouched until
- *   completion.
+ *   completion.  All calls on one comm execute in issue order (the library
+ *   orders its side stream and the caller's streams with events).
  *   Errors (returned now): NOT_INITIALIZED, INVALID_ARGUMENT (buf NULL with
  *   count > 0, unknown dtype), UNSUPPORTED (op != SUM), CUDA.  count == 0 is a
  *   successful no-op.  Cross-rank errors (PROTOCOL, TIMEOUT) surface at

@@ -23,8 +23,8 @@ LIB_PATH = os.path.join(_PKG, "libhfr.so")
 
 SUCCESS, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED, ERR_CUDA, ERR_OUT_OF_MEMORY, ERR_PROTOCOL, \
     ERR_TIMEOUT, ERR_NOT_INITIALIZED, ERR_INTERNAL = range(9)
-ALGO_AUTO, ALGO_FLAT, ALGO_DBT, ALGO_PAIR_DBT = range(4)
-ALGOS = {"auto": ALGO_AUTO, "flat": ALGO_FLAT, "dbt": ALGO_DBT, "pair_dbt": ALGO_PAIR_DBT}
+ALGO_AUTO, ALGO_FLAT, ALGO_DBT, ALGO_PAIR_DBT, ALGO_ONESHOT = range(5)
+ALGOS = {"auto": ALGO_AUTO, "flat": ALGO_FLAT, "dbt": ALGO_DBT, "pair_dbt": ALGO_PAIR_DBT, "oneshot": ALGO_ONESHOT}
 FLOAT32, BFLOAT16 = 0, 1
 SUM = 0
 
@@ -50,7 +50,7 @@ class HfrError(RuntimeError):
 class _Config(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int), ("chunk_elems", ctypes.c_size_t), ("max_ctas", ctypes.c_int),
                 ("threads", ctypes.c_int), ("scale", ctypes.c_float), ("scratch_bytes", ctypes.c_size_t),
-                ("timeout_ms", ctypes.c_int)]
+                ("timeout_ms", ctypes.c_int), ("oneshot_max_bytes", ctypes.c_size_t)]
 
 
 @dataclass
@@ -63,12 +63,13 @@ class Config:
     scale: float = 1.0
     scratch_bytes: int = 0
     timeout_ms: int = 0
+    oneshot_max_bytes: int = 0
 
     def _c(self) -> _Config:
         if self.algo not in ALGOS:
             raise ValueError(f"unknown algo {self.algo!r}")
         return _Config(ALGOS[self.algo], self.chunk_elems, self.max_ctas, self.threads, self.scale,
-                       self.scratch_bytes, self.timeout_ms)
+                       self.scratch_bytes, self.timeout_ms, self.oneshot_max_bytes)
 
 
 _LIB = None
@@ -194,7 +195,7 @@ def _torch_allgather(group):
 
     def ag(send, recv, nbytes, _ctx):
         try:
-            src = torch.frombuffer(ctypes.string_at(send, nbytes), dtype=torch.uint8).clone()
+            src = torch.frombuffer(bytearray(ctypes.string_at(send, nbytes)), dtype=torch.uint8)
             if backend == "nccl":
                 src = src.cuda()
             out = torch.empty(world * nbytes, dtype=torch.uint8, device=src.device)

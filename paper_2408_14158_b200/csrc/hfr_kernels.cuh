@@ -49,6 +49,7 @@ struct TreeNode {
 
 struct Args {
   char* buf[kMaxRanks];    // rank r's data buffer (this call)
+  char* inbox[kMaxRanks];  // rank r's ONESHOT inbox: [2 parities][n sources][slot_bytes]
   float* part[kMaxRanks];  // rank r's fp32 partial slots (tree algos): 2 x part_stride
   Pad* pad[kMaxRanks];
   volatile uint32_t* err;  // host-mapped error word (hfr_status_t), 0 = ok
@@ -57,6 +58,7 @@ struct Args {
   uint64_t sig;            // hash of the call's arguments, compared across ranks
   uint64_t timeout_ns;
   uint64_t part_stride;    // floats per partial slot
+  uint64_t slot_bytes;     // ONESHOT inbox slot size
   uint64_t half_base[2];   // tree algos: element offset of the range each parity works on
   uint64_t half_len[2];
   uint32_t c_lo, c_hi;     // tree algos: global chunk range of this launch
@@ -315,6 +317,85 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
     }
   }
   exit_barrier(a, rank, b);
+}
+
+// ---------------------------------------------------------------------------
+// ONESHOT (small messages): push, then fold locally.
+//
+// CTA b of rank r stores its slice of x_r into slot [epoch&1][r] of every
+// rank's inbox (n-1 NVLink writes), then releases flag entry[b][r] at every
+// rank and waits for entry[b][q] of all q — one cross-rank handoff, carrying
+// the data.  It then folds the n copies of its slice from its LOCAL inbox in
+// rank order 0..n-1 (the same per-element order as FLAT, so the same bits)
+// and writes the result into its own buffer only.  Peers never read this
+// rank's buffer, so any device buffer works without staging, and no exit
+// barrier is needed: a peer reuses a slot parity only two launches later,
+// after the intervening launch's entry barrier proved this CTA done.
+// ---------------------------------------------------------------------------
+template <class E, int NR>
+__global__ void __launch_bounds__(512) hfr_oneshot_kernel(const Args a) {
+  const int rank = a.rank0 + blockIdx.y;
+  const int n = NR > 0 ? NR : a.n;
+  const int b = blockIdx.x;
+  constexpr int K = E::kPerVec;
+  const uint64_t nvec = a.count / K;
+  const uint64_t v0 = nvec * b / gridDim.x, v1 = nvec * (b + 1) / gridDim.x;
+  const uint64_t par = a.epoch & 1;
+  const char* src = a.buf[rank];
+  const bool last = b == (int)gridDim.x - 1;
+  const uint64_t t0 = nvec * K;  // first tail element
+  // the rank's own buffer may be unaligned (any device pointer is accepted):
+  // then this CTA moves its slice element by element
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(a.buf[rank])) & 15) == 0;
+  const uint64_t e_end = last ? a.count : v1 * K;
+  // 1. push
+  if (vec_ok) {
+    for (uint64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) {
+      const uint4 v = ld128(src + i * 16);
+      for (int q = 0; q < n; ++q) st128(a.inbox[q] + (par * n + rank) * a.slot_bytes + i * 16, v);
+    }
+  }
+  for (uint64_t e = (vec_ok ? (last ? t0 : e_end) : v0 * K) + threadIdx.x; e < e_end; e += blockDim.x) {
+    const float x = E::load1(src, e);
+    for (int q = 0; q < n; ++q) E::store1(a.inbox[q] + (par * n + rank) * a.slot_bytes, e, x);
+  }
+  // 2. one handoff: data visible everywhere, then the flag
+  __syncthreads();
+  bool ok = true;
+  if (threadIdx.x < n) {
+    const int q = threadIdx.x;
+    fence_acq_rel_sys();
+    st_relaxed_sys(&a.pad[q]->sig[b][rank], a.sig);
+    st_release_sys(&a.pad[q]->entry[b][rank], a.epoch);
+    ok = wait_ge(a, &a.pad[rank]->entry[b][q], a.epoch);
+    if (ok && ld_relaxed_sys(&a.pad[rank]->sig[b][q]) != a.sig) {
+      raise_error(a, kErrProtocol);
+      ok = false;
+    }
+  }
+  if (!__syncthreads_and(ok)) return;
+  // 3. fold the n local copies in rank order
+  const char* in = a.inbox[rank] + par * n * a.slot_bytes;
+  char* dst = a.buf[rank];
+  if (vec_ok) {
+    for (uint64_t i = v0 + threadIdx.x; i < v1; i += blockDim.x) {
+      float acc[K], t[K];
+      E::widen(ld128(in + i * 16), acc);
+      for (int r = 1; r < n; ++r) {
+        E::widen(ld128(in + r * a.slot_bytes + i * 16), t);
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = __fadd_rn(acc[k], t[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[k] = __fmul_rn(acc[k], a.scale);
+      st128(dst + i * 16, E::narrow(acc));
+    }
+  }
+  for (uint64_t e = (vec_ok ? (last ? t0 : e_end) : v0 * K) + threadIdx.x; e < e_end; e += blockDim.x) {
+    float acc = E::load1(in, e);
+    for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, E::load1(in + r * a.slot_bytes, e));
+    E::store1(dst, e, __fmul_rn(acc, a.scale));
+  }
 }
 
 // ---------------------------------------------------------------------------

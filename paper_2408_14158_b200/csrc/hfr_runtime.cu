@@ -100,6 +100,8 @@ struct hfr_comm_s {
   uint32_t* err_host = nullptr;  // host-mapped error word
   uint32_t* err_dev = nullptr;
   cudaStream_t side = nullptr;
+  cudaEvent_t side_tail = nullptr;  // orders a synchronous call after earlier async ones
+  bool side_busy = false;
   std::vector<cudaEvent_t> ev_pool;
   int num_sms = 148;
   hfr_status_t sticky = HFR_SUCCESS;
@@ -187,10 +189,18 @@ uint64_t fnv(uint64_t h, uint64_t v) {
 
 size_t dtype_size(hfr_dtype_t t) { return t == HFR_BFLOAT16 ? 2 : 4; }
 
-int effective_algo(const hfr_comm_s* c) { return c->cfg.algo == HFR_ALGO_AUTO ? HFR_ALGO_FLAT : c->cfg.algo; }
+// AUTO: ONESHOT up to oneshot_max_bytes, FLAT above; an explicit ONESHOT on a
+// larger message also runs FLAT (same result bits).
+int effective_algo(const hfr_comm_s* c, size_t bytes) {
+  const int a = c->cfg.algo;
+  if (a == HFR_ALGO_AUTO || a == HFR_ALGO_ONESHOT)
+    return bytes <= c->cfg.oneshot_max_bytes ? HFR_ALGO_ONESHOT : HFR_ALGO_FLAT;
+  return a;
+}
 
 hfr_status_t validate_cfg(const hfr_config_t& c) {
-  if (c.algo < HFR_ALGO_AUTO || c.algo > HFR_ALGO_PAIR_DBT) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.algo < HFR_ALGO_AUTO || c.algo > HFR_ALGO_ONESHOT) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.oneshot_max_bytes > (64u << 20)) return HFR_ERR_INVALID_ARGUMENT;
   if (c.chunk_elems % 256 != 0 || c.chunk_elems > (1u << 30)) return HFR_ERR_INVALID_ARGUMENT;
   if (c.max_ctas < 0 || c.max_ctas > kMaxCtas) return HFR_ERR_INVALID_ARGUMENT;
   if (c.threads != 0 && (c.threads < 128 || c.threads > 512 || c.threads % 32 != 0)) return HFR_ERR_INVALID_ARGUMENT;
@@ -204,6 +214,8 @@ void resolve_defaults(hfr_config_t& c) {
   if (c.threads == 0) c.threads = 512;
   if (c.scratch_bytes == 0) c.scratch_bytes = 256ull << 20;
   if (c.timeout_ms == 0) c.timeout_ms = 60000;
+  if (c.oneshot_max_bytes == 0) c.oneshot_max_bytes = 512u << 10;
+  c.oneshot_max_bytes = round_up(c.oneshot_max_bytes, 256);
 }
 
 // ---------------------------------------------------------------------------
@@ -349,20 +361,25 @@ hfr_status_t common_init(hfr_comm_s* c) {
   int lo = 0, hi = 0;
   HFR_CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   HFR_CU(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+  HFR_CU(cudaEventCreateWithFlags(&c->side_tail, cudaEventDisableTiming));
   HFR_TRY(alloc_region(c, sizeof(Pad), &c->pad));
   HFR_TRY(alloc_region(c, c->cfg.scratch_bytes, &c->scratch));
   return HFR_SUCCESS;
 }
 
-// Scratch must hold a staged copy of the message plus the tree partials.
-// Depends only on (count, dtype, algo) so every rank grows in lockstep.
+// Scratch layout per rank: [ONESHOT inbox: 2 x n x oneshot_max][staged copy of
+// the message][tree partials].  Depends only on (count, dtype, algo) so every
+// rank grows in lockstep.
+size_t inbox_bytes(const hfr_comm_s* c) { return round_up(2 * (size_t)c->n * c->cfg.oneshot_max_bytes, kAlign); }
+
 size_t scratch_need(const hfr_comm_s* c, size_t count, hfr_dtype_t dt, int algo) {
-  size_t need = round_up(count * dtype_size(dt), kAlign);
+  size_t need = inbox_bytes(c) + round_up(count * dtype_size(dt), kAlign);
   if (algo == HFR_ALGO_DBT) need += 2 * round_up(count, 64) * 4;
   if (algo == HFR_ALGO_PAIR_DBT) need += 2 * round_up(pair_half(count), 64) * 4;
-  (void)c;
   return need;
 }
+
+char* stage_base(const hfr_comm_s* c, int q) { return c->scratch.base[q] + inbox_bytes(c); }
 
 hfr_status_t ensure_scratch(hfr_comm_s* c, size_t need) {
   if (need <= c->scratch.bytes) return HFR_SUCCESS;
@@ -486,7 +503,7 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   a.chunk = (int)C;
   for (int q = 0; q < c->n; ++q) {
     a.buf[q] = bufs[q];
-    a.part[q] = reinterpret_cast<float*>(c->scratch.base[q] + stage);
+    a.part[q] = reinterpret_cast<float*>(stage_base(c, q) + stage);
   }
   const uint64_t nch = (a.half_len[0] + C - 1) / C;  // half 0 is the longer one
   for (uint64_t lo = 0; lo < std::max<uint64_t>(nch, 1); lo += kMaxChunks) {
@@ -504,6 +521,24 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
     HFR_TRY(launch(c, fn, g, threads, a, s));
   }
   return HFR_SUCCESS;
+}
+
+hfr_status_t run_oneshot(hfr_comm_s* c, char* const* local_bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
+                         cudaStream_t s) {
+  const void* fn = dt == HFR_BFLOAT16 ? (const void*)hfr_oneshot_kernel<BF16, 0> : (const void*)hfr_oneshot_kernel<F32, 0>;
+  const uint64_t per = dt == HFR_BFLOAT16 ? 8 : 4;
+  const uint64_t nvec = count / per;
+  // small grids: one CTA per 2048 vectors (32 KiB), at least n threads
+  const int min_thr = 32 * ((c->n + 31) / 32);
+  const int threads = (int)std::max<uint64_t>(min_thr, std::min<uint64_t>(c->cfg.threads, round_up(std::max<uint64_t>(nvec, 1), 32)));
+  int g = 0;
+  HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>((nvec + 2047) / 2048 + 1, kMaxCtas), &g));
+  Args a;
+  base_args(c, a, count, fnv(sig, (uint64_t)g * 1315423911ull + threads));
+  a.slot_bytes = c->cfg.oneshot_max_bytes;
+  for (int q = 0; q < c->n; ++q) a.inbox[q] = c->scratch.base[q];
+  for (int q = 0; q < c->local; ++q) a.buf[c->virt ? q : c->rank] = local_bufs[q];
+  return launch(c, fn, g, threads, a, s);
 }
 
 hfr_status_t run_copy(hfr_comm_s* c, char* dst, const char* src, uint64_t bytes, cudaStream_t s) {
@@ -552,7 +587,7 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
   if (dt != HFR_FLOAT32 && dt != HFR_BFLOAT16) return HFR_ERR_INVALID_ARGUMENT;
   if (op != HFR_SUM) return HFR_ERR_UNSUPPORTED;
   if (c->sticky != HFR_SUCCESS) return c->sticky;
-  const int algo = effective_algo(c);
+  const int algo = effective_algo(c, count * dtype_size(dt));
   if (algo == HFR_ALGO_PAIR_DBT && c->n % 2 != 0) return HFR_ERR_UNSUPPORTED;
   for (int q = 0; q < c->local; ++q)
     if (count > 0 && !local_bufs[q]) return HFR_ERR_INVALID_ARGUMENT;
@@ -566,6 +601,12 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     HFR_CU(cudaStreamWaitEvent(c->side, ready, 0));
     c->ev_pool.push_back(ready);
     s = c->side;
+  } else if (c->side_busy) {
+    // keep every call of this comm in issue order: the caller's stream waits
+    // for the asynchronous calls issued before this one
+    HFR_CU(cudaEventRecord(c->side_tail, c->side));
+    HFR_CU(cudaStreamWaitEvent(user, c->side_tail, 0));
+    c->side_busy = false;
   }
   if (count > 0) {
     const size_t esz = dtype_size(dt);
@@ -578,24 +619,30 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     bool zero_copy = aligned && (c->virt || find_region(c, local_bufs[0], bytes, &reg));
     uint64_t offset = zero_copy && reg ? (uint64_t)(local_bufs[0] - reg->base[c->rank]) : 0;
     HFR_TRY(ensure_scratch(c, scratch_need(c, count, dt, algo)));
-
+    uint64_t sig = 1469598103934665603ull;
+    sig = fnv(sig, count);
+    sig = fnv(sig, (uint64_t)dt | ((uint64_t)op << 8) | ((uint64_t)algo << 16));
+    uint32_t sbits;
+    memcpy(&sbits, &c->cfg.scale, 4);
+    sig = fnv(sig, sbits);
+    if (algo == HFR_ALGO_ONESHOT) {
+      // peers never touch this rank's buffer: no staging, any device pointer
+      HFR_TRY(run_oneshot(c, local_bufs, count, dt, sig, s));
+      goto done;
+    }
+    {
     char* bufs[kMaxRanks] = {};
     if (zero_copy) {
       for (int q = 0; q < c->n; ++q) bufs[q] = c->virt ? local_bufs[q] : reg->base[q] + offset;
     } else {
-      for (int q = 0; q < c->n; ++q) bufs[q] = c->scratch.base[q];
+      for (int q = 0; q < c->n; ++q) bufs[q] = stage_base(c, q);
       for (int q = 0; q < c->local; ++q) {
         const int r = c->virt ? q : c->rank;
-        HFR_TRY(run_copy(c, c->scratch.base[r], local_bufs[q], bytes, s));
+        HFR_TRY(run_copy(c, stage_base(c, r), local_bufs[q], bytes, s));
       }
     }
-    uint64_t sig = 1469598103934665603ull;
-    sig = fnv(sig, count);
-    sig = fnv(sig, (uint64_t)dt | ((uint64_t)op << 8) | ((uint64_t)algo << 16) | ((uint64_t)zero_copy << 24));
+    sig = fnv(sig, (uint64_t)zero_copy);
     sig = fnv(sig, algo == HFR_ALGO_FLAT ? 0 : c->cfg.chunk_elems);
-    uint32_t sbits;
-    memcpy(&sbits, &c->cfg.scale, 4);
-    sig = fnv(sig, sbits);
     sig = fnv(sig, offset);
     if (algo == HFR_ALGO_FLAT) {
       HFR_TRY(run_flat(c, bufs, count, dt, sig, s));
@@ -605,11 +652,14 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     if (!zero_copy) {
       for (int q = 0; q < c->local; ++q) {
         const int r = c->virt ? q : c->rank;
-        HFR_TRY(run_copy(c, local_bufs[q], c->scratch.base[r], bytes, s));
+        HFR_TRY(run_copy(c, local_bufs[q], stage_base(c, r), bytes, s));
       }
     }
+    }
   }
+done:
   if (req) {
+    c->side_busy = true;
     cudaEvent_t done = take_event(c);
     if (!done) return HFR_ERR_CUDA;
     HFR_CU(cudaEventRecord(done, s));
@@ -689,6 +739,7 @@ hfr_status_t hfr_comm_set_config(hfr_comm_t c, const hfr_config_t* cfg) {
   HFR_TRY(validate_cfg(n));
   n.scratch_bytes = c->cfg.scratch_bytes;
   n.timeout_ms = c->cfg.timeout_ms;
+  n.oneshot_max_bytes = c->cfg.oneshot_max_bytes;
   resolve_defaults(n);
   c->cfg = n;
   return HFR_SUCCESS;
@@ -813,6 +864,7 @@ hfr_status_t hfr_finalize(hfr_comm_t c) {
     close_region(c, c->scratch);
     close_region(c, c->pad);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    if (c->side_tail) cudaEventDestroy(c->side_tail);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->err_host) cudaFreeHost(c->err_host);
   }

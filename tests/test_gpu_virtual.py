@@ -61,7 +61,7 @@ def check(outs, want, what):
         assert_bit_exact(g, want, f"{what} rank {r}")
 
 
-ALGOS = ["flat", "dbt", "pair_dbt"]
+ALGOS = ["flat", "oneshot", "dbt", "pair_dbt"]
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8])
@@ -129,7 +129,7 @@ def test_golden_order_examples_on_gpu(hfr, algo):
     import os
     cases = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "order_examples.json")))["cases"]
     for case in cases:
-        if case["algo"] != algo:
+        if case["algo"] != algo and not (algo == "oneshot" and case["algo"] == "flat"):
             continue
         xs0 = [np.array(v, dtype=np.float32) for v in case["inputs"]]
         # element j of the example -> chunk j (256 elements each, all equal)

@@ -80,24 +80,20 @@ def main():
     comm = hfr.Comm.init(device=local, config=hfr.Config(algo=a.algo, max_ctas=a.max_ctas, scale=1.0 / world))
     ddp = HaiScaleDDP(comm, numels, torch.bfloat16, bucket_bytes=a.bucket_mib << 20)
     T = a.tokens
-    max_out = max(o for _, o, _ in params)
-    max_in = max(i for _, _, i in params if i <= 65536)
     g = torch.Generator(device=dev).manual_seed(3000 + rank)
-    dY = torch.randn(T, max_out, device=dev, dtype=torch.bfloat16, generator=g)
-    X = torch.randn(T, max_in, device=dev, dtype=torch.bfloat16, generator=g)
-    W = {}
-    for _, o, i in params:
-        if (o, i) not in W and o > 1 and i <= 65536:
-            W[(o, i)] = torch.randn(o, i, device=dev, dtype=torch.bfloat16, generator=g) * 0.02
-    dX = torch.empty(T, max_in, device=dev, dtype=torch.bfloat16)
+    gemm = [(o, i) for _, o, i in params if o > 1 and i <= 65536]
+    dY = {o: torch.randn(T, o, device=dev, dtype=torch.bfloat16, generator=g) for o in sorted({o for o, _ in gemm})}
+    X = {i: torch.randn(T, i, device=dev, dtype=torch.bfloat16, generator=g) for i in sorted({i for _, i in gemm})}
+    W = {oi: torch.randn(*oi, device=dev, dtype=torch.bfloat16, generator=g) * 0.02 for oi in sorted(set(gemm))}
+    dX = {i: torch.empty(T, i, device=dev, dtype=torch.bfloat16) for i in X}
     compute = torch.cuda.current_stream()
 
     def backward(with_comm: bool):
         for idx, (_, o, i) in enumerate(params):
             gv = ddp.grad(idx)
             if o > 1 and i <= 65536:
-                torch.matmul(dY[:, :o].t(), X[:, :i], out=gv.view(o, i))      # wgrad into the bucket arena
-                torch.matmul(dY[:, :o], W[(o, i)], out=dX[:, :i])              # dgrad (load)
+                torch.matmul(dY[o].t(), X[i], out=gv.view(o, i))      # wgrad into the bucket arena
+                torch.matmul(dY[o], W[(o, i)], out=dX[i])              # dgrad (load)
             else:
                 gv.fill_(1.0 / (idx + 1))                                      # norms / pad
             if with_comm:
