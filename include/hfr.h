@@ -150,6 +150,10 @@ hfr_status_t hfr_register(hfr_comm_t comm, void* ptr, size_t bytes);
  *   Ownership: caller owns buf; it must stay allocated and untouched until
  *   completion.  All calls on one comm execute in issue order (the library
  *   orders its side stream and the caller's streams with events).
+ *   CUDA graphs: calls may be captured (stream capture) and replayed; launch
+ *   epochs live in device memory.  The first call of a given size must run
+ *   uncaptured (it may grow the scratch, which is collective); a captured
+ *   call that would need more scratch returns UNSUPPORTED.
  *   Errors (returned now): NOT_INITIALIZED, INVALID_ARGUMENT (buf NULL with
  *   count > 0, unknown dtype), UNSUPPORTED (op != SUM), CUDA.  count == 0 is a
  *   successful no-op.  Cross-rank errors (PROTOCOL, TIMEOUT) surface at

@@ -25,7 +25,9 @@ constexpr int kMaxChunks = 65536;
 // Peer-mapped signal pad, one per rank (DESIGN.md §5 "HBM layout").
 // entry/sig/exit[b][q] are written by rank q's CTA b; up/down/pdown[c] are the
 // per-chunk tree flags (c = chunk index local to the launch).  All values are
-// launch epochs, strictly increasing per comm, so nothing is ever reset.
+// launch epochs, strictly increasing per rank, so nothing is ever reset.  The
+// epoch lives in device memory (launch_epoch), not in the kernel arguments,
+// so captured CUDA graphs replay correctly.
 struct Pad {
   uint64_t entry[kMaxCtas][kMaxRanks];
   uint64_t sig[kMaxCtas][kMaxRanks];
@@ -33,6 +35,8 @@ struct Pad {
   uint64_t up[2][kMaxChunks];   // child partial for chunk c landed in slot s
   uint64_t down[kMaxChunks];    // final chunk c landed in my buffer (from tree parent)
   uint64_t pdown[kMaxChunks];   // final chunk c of my other half landed (from pair partner)
+  uint64_t launch_epoch;        // epoch of the last completed launch on this rank
+  uint32_t done_ctas;           // CTAs of the current launch that have finished
 };
 
 // One node of a double binary tree (reading R9/R10).  Children are sorted by
@@ -54,7 +58,6 @@ struct Args {
   Pad* pad[kMaxRanks];
   volatile uint32_t* err;  // host-mapped error word (hfr_status_t), 0 = ok
   uint64_t count;          // elements per rank
-  uint64_t epoch;
   uint64_t sig;            // hash of the call's arguments, compared across ranks
   uint64_t timeout_ns;
   uint64_t part_stride;    // floats per partial slot
@@ -94,6 +97,28 @@ __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
+}
+
+// Launch epoch.  Every CTA reads the rank's launch_epoch at entry (+1 = this
+// launch); the last CTA of the launch to finish publishes it.  A CTA can only
+// finish after reading, so every CTA of a launch sees the same value whatever
+// the residency, and the next launch (stream order) sees the update.
+__device__ __forceinline__ uint64_t begin_epoch(Pad* mine) {
+  __shared__ uint64_t s_epoch;
+  if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile uint64_t*>(&mine->launch_epoch) + 1;
+  __syncthreads();
+  return s_epoch;
+}
+__device__ __forceinline__ void end_epoch(Pad* mine, uint64_t e) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&mine->done_ctas, 1u) == gridDim.x - 1) {
+      mine->done_ctas = 0;
+      *reinterpret_cast<volatile uint64_t*>(&mine->launch_epoch) = e;
+      __threadfence();
+    }
+  }
 }
 
 // 128-bit data movement.  Loads skip L1 allocation (each byte is read once);
@@ -140,13 +165,13 @@ __device__ __noinline__ bool wait_ge(const Args& a, const uint64_t* p, uint64_t 
 // publishes (sig, epoch) to CTA b of every rank and waits for all of them.
 // When it returns true every rank has entered this launch, so every rank's
 // prior stream work on its buffers is complete.  Caller must __syncthreads().
-__device__ __forceinline__ bool entry_barrier(const Args& a, int rank, int b) {
+__device__ __forceinline__ bool entry_barrier(const Args& a, int rank, int b, uint64_t e) {
   bool ok = true;
   const int q = threadIdx.x;
   if (q < a.n) {
     st_relaxed_sys(&a.pad[q]->sig[b][rank], a.sig);
-    st_release_sys(&a.pad[q]->entry[b][rank], a.epoch);
-    ok = wait_ge(a, &a.pad[rank]->entry[b][q], a.epoch);
+    st_release_sys(&a.pad[q]->entry[b][rank], e);
+    ok = wait_ge(a, &a.pad[rank]->entry[b][q], e);
     if (ok && ld_relaxed_sys(&a.pad[rank]->sig[b][q]) != a.sig) {
       raise_error(a, kErrProtocol);
       ok = false;
@@ -157,13 +182,13 @@ __device__ __forceinline__ bool entry_barrier(const Args& a, int rank, int b) {
 
 // a5 completion: CTA b tells CTA b of every rank that all its loads from and
 // stores to that rank are done, and waits for the same from everyone.
-__device__ __forceinline__ void exit_barrier(const Args& a, int rank, int b) {
+__device__ __forceinline__ void exit_barrier(const Args& a, int rank, int b, uint64_t e) {
   __syncthreads();
   const int q = threadIdx.x;
   if (q < a.n) {
     fence_acq_rel_sys();
-    st_relaxed_sys(&a.pad[q]->exit[b][rank], a.epoch);
-    wait_ge(a, &a.pad[rank]->exit[b][q], a.epoch);
+    st_relaxed_sys(&a.pad[q]->exit[b][rank], e);
+    wait_ge(a, &a.pad[rank]->exit[b][q], e);
   }
   __syncthreads();
 }
@@ -287,7 +312,8 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
   const int rank = a.rank0 + blockIdx.y;
   const int n = NR > 0 ? NR : a.n;
   const int b = blockIdx.x;
-  if (entry_barrier(a, rank, b)) {
+  const uint64_t e = begin_epoch(a.pad[rank]);
+  if (entry_barrier(a, rank, b, e)) {
     constexpr int K = E::kPerVec;
     constexpr int U = NR > 4 ? 2 : (NR > 2 ? 3 : 4);
     const uint64_t nvec = a.count / K;
@@ -309,14 +335,15 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
     // ragged tail (< K elements) — owned by the last rank, CTA 0
     const uint64_t t0 = nvec * K;
     if (rank == n - 1 && b == 0 && threadIdx.x < a.count - t0) {
-      const uint64_t e = t0 + threadIdx.x;
-      float acc = E::load1(a.buf[0], e);
-      for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, E::load1(a.buf[r], e));
+      const uint64_t el = t0 + threadIdx.x;
+      float acc = E::load1(a.buf[0], el);
+      for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, E::load1(a.buf[r], el));
       acc = __fmul_rn(acc, a.scale);
-      for (int r = 0; r < n; ++r) E::store1(a.buf[r], e, acc);
+      for (int r = 0; r < n; ++r) E::store1(a.buf[r], el, acc);
     }
   }
-  exit_barrier(a, rank, b);
+  exit_barrier(a, rank, b, e);
+  end_epoch(a.pad[rank], e);
 }
 
 // ---------------------------------------------------------------------------
@@ -340,7 +367,8 @@ __global__ void __launch_bounds__(512) hfr_oneshot_kernel(const Args a) {
   constexpr int K = E::kPerVec;
   const uint64_t nvec = a.count / K;
   const uint64_t v0 = nvec * b / gridDim.x, v1 = nvec * (b + 1) / gridDim.x;
-  const uint64_t par = a.epoch & 1;
+  const uint64_t ep = begin_epoch(a.pad[rank]);
+  const uint64_t par = ep & 1;
   const char* src = a.buf[rank];
   const bool last = b == (int)gridDim.x - 1;
   const uint64_t t0 = nvec * K;  // first tail element
@@ -366,8 +394,8 @@ __global__ void __launch_bounds__(512) hfr_oneshot_kernel(const Args a) {
     const int q = threadIdx.x;
     fence_acq_rel_sys();
     st_relaxed_sys(&a.pad[q]->sig[b][rank], a.sig);
-    st_release_sys(&a.pad[q]->entry[b][rank], a.epoch);
-    ok = wait_ge(a, &a.pad[rank]->entry[b][q], a.epoch);
+    st_release_sys(&a.pad[q]->entry[b][rank], ep);
+    ok = wait_ge(a, &a.pad[rank]->entry[b][q], ep);
     if (ok && ld_relaxed_sys(&a.pad[rank]->sig[b][q]) != a.sig) {
       raise_error(a, kErrProtocol);
       ok = false;
@@ -396,6 +424,7 @@ __global__ void __launch_bounds__(512) hfr_oneshot_kernel(const Args a) {
     for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, E::load1(in + r * a.slot_bytes, e));
     E::store1(dst, e, __fmul_rn(acc, a.scale));
   }
+  end_epoch(a.pad[rank], ep);
 }
 
 // ---------------------------------------------------------------------------
@@ -447,7 +476,8 @@ template <class E, bool PAIR>
 __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
   const int rank = a.rank0 + blockIdx.y;
   const int b = blockIdx.x;
-  const bool ok = entry_barrier(a, rank, b);
+  const uint64_t ep = begin_epoch(a.pad[rank]);
+  const bool ok = entry_barrier(a, rank, b, ep);
   if (!ok) return;
 
   const int h = PAIR ? (rank & 1) : 0;
@@ -467,7 +497,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     const TreeNode nd = a.tree[c & 1][me];
     const uint32_t lc = (uint32_t)(c - a.c_lo);
     bool got = true;
-    if (threadIdx.x < nd.nchild) got = wait_ge(a, &mypad->up[threadIdx.x][lc], a.epoch);
+    if (threadIdx.x < nd.nchild) got = wait_ge(a, &mypad->up[threadIdx.x][lc], ep);
     if (!__syncthreads_and(got)) return;
 
     const uint64_t e0 = c * C, e1 = (e0 + C < len) ? e0 + C : len;  // offsets within the half
@@ -539,10 +569,10 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     if (threadIdx.x == 0) {
       fence_acq_rel_sys();
       if (root) {
-        for (int k = 0; k < nd.nchild; ++k) st_relaxed_sys(&a.pad[member(nd.child[k])]->down[lc], a.epoch);
-        if constexpr (PAIR) st_relaxed_sys(&a.pad[partner]->pdown[lc], a.epoch);
+        for (int k = 0; k < nd.nchild; ++k) st_relaxed_sys(&a.pad[member(nd.child[k])]->down[lc], ep);
+        if constexpr (PAIR) st_relaxed_sys(&a.pad[partner]->pdown[lc], ep);
       } else {
-        st_relaxed_sys(&a.pad[member(nd.parent)]->up[nd.slot][lc], a.epoch);
+        st_relaxed_sys(&a.pad[member(nd.parent)]->up[nd.slot][lc], ep);
       }
     }
   }
@@ -553,7 +583,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     if (nd.parent < 0) continue;  // the root already pushed its final chunk
     const uint32_t lc = (uint32_t)(c - a.c_lo);
     bool got = true;
-    if (threadIdx.x == 0) got = wait_ge(a, &mypad->down[lc], a.epoch);
+    if (threadIdx.x == 0) got = wait_ge(a, &mypad->down[lc], ep);
     if (!__syncthreads_and(got)) return;
     if (nd.nchild == 0 && !PAIR) continue;
     const uint64_t e0 = c * C, e1 = (e0 + C < len) ? e0 + C : len;
@@ -579,8 +609,8 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     __syncthreads();
     if (threadIdx.x == 0) {
       fence_acq_rel_sys();
-      for (int k = 0; k < nd.nchild; ++k) st_relaxed_sys(&a.pad[member(nd.child[k])]->down[lc], a.epoch);
-      if constexpr (PAIR) st_relaxed_sys(&a.pad[partner]->pdown[lc], a.epoch);
+      for (int k = 0; k < nd.nchild; ++k) st_relaxed_sys(&a.pad[member(nd.child[k])]->down[lc], ep);
+      if constexpr (PAIR) st_relaxed_sys(&a.pad[partner]->pdown[lc], ep);
     }
   }
 
@@ -590,9 +620,10 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     const uint64_t onch = (olen + C - 1) / C;
     const uint64_t oend = onch < a.c_hi ? onch : a.c_hi;
     for (uint64_t c = a.c_lo + b; c < oend; c += gridDim.x) {
-      if (threadIdx.x == 0) wait_ge(a, &mypad->pdown[(uint32_t)(c - a.c_lo)], a.epoch);
+      if (threadIdx.x == 0) wait_ge(a, &mypad->pdown[(uint32_t)(c - a.c_lo)], ep);
     }
   }
+  end_epoch(mypad, ep);
 }
 
 // ---------------------------------------------------------------------------
@@ -613,7 +644,8 @@ __global__ void __launch_bounds__(1024) hfr_copy_kernel(char* dst, const char* s
 
 __global__ void hfr_barrier_kernel(const Args a) {
   const int rank = a.rank0 + blockIdx.y;
-  entry_barrier(a, rank, 0);
+  const uint64_t e = begin_epoch(a.pad[rank]);
+  if (entry_barrier(a, rank, 0, e)) end_epoch(a.pad[rank], e);
 }
 
 }  // namespace hfr

@@ -417,7 +417,7 @@ const void* tree_fn(bool pair) {
 }
 
 hfr_status_t launch(hfr_comm_s* c, const void* fn, int grid_x, int threads, Args& a, cudaStream_t s) {
-  a.epoch = ++c->epoch;
+  ++c->epoch;  // host mirror (stats only): kernels keep their epoch in device memory
   void* params[] = {&a};
   dim3 grid(grid_x, c->local), block(threads);
   cudaError_t e;
@@ -593,6 +593,12 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     if (count > 0 && !local_bufs[q]) return HFR_ERR_INVALID_ARGUMENT;
   DeviceGuard guard(c->dev);
 
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  HFR_CU(cudaStreamIsCapturing(user, &cap));
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  if (capturing && count > 0 && scratch_need(c, count, dt, algo) > c->scratch.bytes)
+    return HFR_ERR_UNSUPPORTED;  // scratch growth is collective and synchronous: call once before capturing
+
   cudaStream_t s = user;
   if (req) {
     cudaEvent_t ready = take_event(c);
@@ -601,7 +607,7 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     HFR_CU(cudaStreamWaitEvent(c->side, ready, 0));
     c->ev_pool.push_back(ready);
     s = c->side;
-  } else if (c->side_busy) {
+  } else if (c->side_busy && !capturing) {
     // keep every call of this comm in issue order: the caller's stream waits
     // for the asynchronous calls issued before this one
     HFR_CU(cudaEventRecord(c->side_tail, c->side));

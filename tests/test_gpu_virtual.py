@@ -167,3 +167,30 @@ def test_bf16_exhaustive_n2_sample(hfr):
     fa, fb = O.widen(a), O.widen(b)
     want = torch.from_numpy(fa + fb).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     check(outs, want, "bf16 n=2")
+
+
+@pytest.mark.parametrize("algo", ALGOS)
+def test_cuda_graph_replay(hfr, algo):
+    """Captured allreduces replay correctly (device-side launch epochs): k
+    replays of one captured in-place allreduce == the oracle applied k times."""
+    n, N = 4, 20_000 + 3
+    comm = comm_for(hfr, n)
+    comm.set_config(hfr.Config(algo=algo, chunk_elems=512, scale=0.25))
+    xs = gen.rank_inputs(n, N, gen.FP32, "normal", seed_base=66)
+    bufs = comm.empty(N, torch.float32)
+    for b, x in zip(bufs, xs):
+        b.copy_(to_torch(x, "cuda:0"))
+    comm.allreduce_virtual(bufs)          # uncaptured first call (sizes the scratch)
+    torch.cuda.synchronize()
+    want = O.allreduce(xs, algo, chunk_elems=512, scale=0.25)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            comm.allreduce_virtual(bufs)
+    for _ in range(3):
+        g.replay()
+        want = O.allreduce(want, algo, chunk_elems=512, scale=0.25)
+    torch.cuda.synchronize()
+    assert comm.status() == hfr.SUCCESS
+    check([to_numpy(b) for b in bufs], want[0], f"graph {algo}")

@@ -32,6 +32,7 @@ def main():
     p.add_argument("--threads", default="0")
     p.add_argument("--iters", type=int, default=0)
     p.add_argument("--nccl", action="store_true")
+    p.add_argument("--graph", action="store_true", help="time `iters` calls captured in one CUDA graph")
     p.add_argument("--out", default="")
     a = p.parse_args()
 
@@ -73,14 +74,30 @@ def main():
     def timeit(fn, iters):
         for _ in range(3):
             fn()
+        torch.cuda.synchronize()
+        run = None
+        if a.graph:
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream()
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                with torch.cuda.graph(g, stream=cs):
+                    for _ in range(iters):
+                        fn()
+            torch.cuda.synchronize()
+            g.replay()  # warm
+            run = g.replay
         if multi:
             dist.barrier()
         comm.barrier(stream)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(iters):
-            fn()
+        if run is not None:
+            run()
+        else:
+            for _ in range(iters):
+                fn()
         e1.record(stream)
         torch.cuda.synchronize()
         return mx(e0.elapsed_time(e1) / 1e3 / iters)
@@ -108,13 +125,13 @@ def main():
             st = comm.status()
             if st != hfr.SUCCESS:
                 raise SystemExit(f"hfr error {hfr.status_string(st)}")
-            emit({"impl": "hfr", "n": n, "virtual": not multi, "dtype": a.dtype, "bytes": size, "algo": algo,
+            emit({"impl": "hfr", "n": n, "virtual": not multi, "graph": a.graph, "dtype": a.dtype, "bytes": size, "algo": algo,
                   "chunk": chunk, "ctas": ctas, "threads": thr, "us": t * 1e6,
                   "busbw": size / t * 2 * (n - 1) / n / 1e9, "algbw": size / t / 1e9})
         if multi and a.nccl:
             t_ = torch.empty(cnt, dtype=tdt, device=dev).normal_()
             tn = timeit(lambda: dist.all_reduce(t_), iters)
-            emit({"impl": "nccl", "n": n, "dtype": a.dtype, "bytes": size, "us": tn * 1e6,
+            emit({"impl": "nccl", "n": n, "graph": a.graph, "dtype": a.dtype, "bytes": size, "us": tn * 1e6,
                   "busbw": size / tn * 2 * (n - 1) / n / 1e9, "algbw": size / tn / 1e9,
                   "env": {k: v for k, v in os.environ.items() if k.startswith("NCCL_")}})
             del t_
