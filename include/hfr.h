@@ -65,13 +65,20 @@ typedef enum {
  *            a push-only P2P schedule over the GPUs; chunk c rides tree c mod 2.
  *   PAIR_DBT "HFReduce with NVLink": pair (2k,2k+1) reduce,
  *            tree over the n/2 pair partials per half, pair all-gather.
+ *   CE       copy-engine two-shot (the paper's "No GPU Kernel Overhead",
+ *            PAPER.md:375): peers' shards are PULLED by the copy engines,
+ *            cross-rank ordering uses stream memory operations (no SM spins),
+ *            and only a short local fold kernel runs on the SMs — for
+ *            overlapping with compute (DDP).  Same result bits as FLAT.
+ *            Needs peer-mapped buffers on a real comm; otherwise runs FLAT.
  *   AUTO     ONESHOT up to oneshot_max_bytes, FLAT above. */
 typedef enum {
     HFR_ALGO_AUTO = 0,
     HFR_ALGO_FLAT = 1,
     HFR_ALGO_DBT = 2,
     HFR_ALGO_PAIR_DBT = 3,
-    HFR_ALGO_ONESHOT = 4
+    HFR_ALGO_ONESHOT = 4,
+    HFR_ALGO_CE = 5
 } hfr_algo_t;
 
 /* All-gather callback used ONLY by the collective setup calls (hfr_init,

@@ -239,7 +239,7 @@ def fold_pairfirst(xs, chunk_elems: int, scale: float = 1.0) -> np.ndarray:
 
 def allreduce(xs, algo: str = "flat", chunk_elems: int = 1 << 16, scale: float = 1.0):
     """Every rank's output (identical bytes on all ranks) for the given order."""
-    if algo in ("flat", "oneshot", "auto"):
+    if algo in ("flat", "oneshot", "auto", "ce"):
         y = fold_ascending(xs, scale)
     elif algo == "dbt":
         y = fold_tree(xs, chunk_elems, scale)

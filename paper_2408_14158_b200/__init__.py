@@ -23,8 +23,9 @@ LIB_PATH = os.path.join(_PKG, "libhfr.so")
 
 SUCCESS, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED, ERR_CUDA, ERR_OUT_OF_MEMORY, ERR_PROTOCOL, \
     ERR_TIMEOUT, ERR_NOT_INITIALIZED, ERR_INTERNAL = range(9)
-ALGO_AUTO, ALGO_FLAT, ALGO_DBT, ALGO_PAIR_DBT, ALGO_ONESHOT = range(5)
-ALGOS = {"auto": ALGO_AUTO, "flat": ALGO_FLAT, "dbt": ALGO_DBT, "pair_dbt": ALGO_PAIR_DBT, "oneshot": ALGO_ONESHOT}
+ALGO_AUTO, ALGO_FLAT, ALGO_DBT, ALGO_PAIR_DBT, ALGO_ONESHOT, ALGO_CE = range(6)
+ALGOS = {"auto": ALGO_AUTO, "flat": ALGO_FLAT, "dbt": ALGO_DBT, "pair_dbt": ALGO_PAIR_DBT, "oneshot": ALGO_ONESHOT,
+         "ce": ALGO_CE}
 FLOAT32, BFLOAT16 = 0, 1
 SUM = 0
 

@@ -23,18 +23,20 @@ constexpr int kMaxCtas = 1024;
 constexpr int kMaxChunks = 65536;
 
 // Peer-mapped signal pad, one per rank (DESIGN.md §5 "HBM layout").
-// entry/sig/exit[b][q] are written by rank q's CTA b; up/down/pdown[c] are the
+// entry/exit[b][q] are written by rank q's CTA b; up/down/pdown[c] are the
 // per-chunk tree flags (c = chunk index local to the launch).  All values are
 // launch epochs, strictly increasing per rank, so nothing is ever reset.  The
 // epoch lives in device memory (launch_epoch), not in the kernel arguments,
 // so captured CUDA graphs replay correctly.
 struct Pad {
-  uint64_t entry[kMaxCtas][kMaxRanks];
-  uint64_t sig[kMaxCtas][kMaxRanks];
+  uint64_t entry[kMaxCtas][kMaxRanks];  // packed (epoch << 32 | sig32)
   uint64_t exit[kMaxCtas][kMaxRanks];
   uint64_t up[2][kMaxChunks];   // child partial for chunk c landed in slot s
   uint64_t down[kMaxChunks];    // final chunk c landed in my buffer (from tree parent)
   uint64_t pdown[kMaxChunks];   // final chunk c of my other half landed (from pair partner)
+  uint64_t ce_ready[kMaxRanks]; // CE schedule: rank q's buffer is ready (stream memop flags)
+  uint64_t ce_done[kMaxRanks];  //   rank q's result shard is final
+  uint64_t ce_exit[kMaxRanks];  //   rank q finished pulling from every peer
   uint64_t launch_epoch;        // epoch of the last completed launch on this rank
   uint32_t done_ctas;           // CTAs of the current launch that have finished
 };
@@ -160,22 +162,35 @@ __device__ __noinline__ bool wait_ge(const Args& a, const uint64_t* p, uint64_t 
   }
 }
 
+// Handshake flags pack (launch epoch << 32 | 32-bit argument signature) into
+// one 64-bit word, so publishing needs a single store and no fence.
+__device__ __forceinline__ uint64_t pack_flag(uint64_t e, uint64_t sig) {
+  return (e << 32) | (uint32_t)(sig ^ (sig >> 32));
+}
+
+// Wait for the packed flag of epoch e at *p and check the signature.
+__device__ __forceinline__ bool wait_flag(const Args& a, const uint64_t* p, uint64_t e) {
+  if (!wait_ge(a, p, e << 32)) return false;
+  if (ld_relaxed_sys(p) != pack_flag(e, a.sig)) {
+    raise_error(a, kErrProtocol);
+    return false;
+  }
+  return true;
+}
+
 // a0 "trigger and entry handshake" ("wait for chunk-i
 // transfer finished in this node", made a device barrier): CTA b of `rank`
-// publishes (sig, epoch) to CTA b of every rank and waits for all of them.
+// publishes (epoch, sig) to CTA b of every rank and waits for all of them.
 // When it returns true every rank has entered this launch, so every rank's
-// prior stream work on its buffers is complete.  Caller must __syncthreads().
+// prior stream work on its buffers is complete (kernel boundaries order it;
+// no fence is needed before the flag).  Ranks that disagree on the call's
+// arguments see a signature mismatch -> HFR_ERR_PROTOCOL.
 __device__ __forceinline__ bool entry_barrier(const Args& a, int rank, int b, uint64_t e) {
   bool ok = true;
   const int q = threadIdx.x;
   if (q < a.n) {
-    st_relaxed_sys(&a.pad[q]->sig[b][rank], a.sig);
-    st_release_sys(&a.pad[q]->entry[b][rank], e);
-    ok = wait_ge(a, &a.pad[rank]->entry[b][q], e);
-    if (ok && ld_relaxed_sys(&a.pad[rank]->sig[b][q]) != a.sig) {
-      raise_error(a, kErrProtocol);
-      ok = false;
-    }
+    st_relaxed_sys(&a.pad[q]->entry[b][rank], pack_flag(e, a.sig));
+    ok = wait_flag(a, &a.pad[rank]->entry[b][q], e);
   }
   return __syncthreads_and(ok);
 }
@@ -392,14 +407,9 @@ __global__ void __launch_bounds__(512) hfr_oneshot_kernel(const Args a) {
   bool ok = true;
   if (threadIdx.x < n) {
     const int q = threadIdx.x;
-    fence_acq_rel_sys();
-    st_relaxed_sys(&a.pad[q]->sig[b][rank], a.sig);
-    st_release_sys(&a.pad[q]->entry[b][rank], ep);
-    ok = wait_ge(a, &a.pad[rank]->entry[b][q], ep);
-    if (ok && ld_relaxed_sys(&a.pad[rank]->sig[b][q]) != a.sig) {
-      raise_error(a, kErrProtocol);
-      ok = false;
-    }
+    fence_acq_rel_sys();  // this CTA's pushes are visible before the flag
+    st_relaxed_sys(&a.pad[q]->entry[b][rank], pack_flag(ep, a.sig));
+    ok = wait_flag(a, &a.pad[rank]->entry[b][q], ep);
   }
   if (!__syncthreads_and(ok)) return;
   // 3. fold the n local copies in rank order
@@ -505,43 +515,58 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     const bool root = nd.parent < 0;
     char* const pbuf = PAIR ? a.buf[partner] : nullptr;
     float* const dst_part = root ? nullptr : a.part[member(nd.parent)] + (uint64_t)nd.slot * a.part_stride;
-    for (uint64_t v = threadIdx.x; v < nv; v += blockDim.x) {
-      const uint64_t e = e0 + v * 8;
-      float acc[8], t[8];
-      // node value x_v (PAIR: fl32(x_2k + x_2k+1), lower rank first)
-      float xv[8];
-      load8<E>(mybuf, base + e, xv);
-      if constexpr (PAIR) {
-        float xp[8];
-        load8<E>(pbuf, base + e, xp);
+    // TU units of 8 elements per thread per iteration: every load of the TU
+    // units (x_v, the partner's x, the children's partials) is issued before
+    // the first add, so a CTA keeps TU x (2..4) x 32 B per thread in flight.
+    constexpr int TU = 2;
+    const int nchild = nd.nchild, self_pos = nd.self_pos;
+    for (uint64_t v0 = threadIdx.x; v0 < nv; v0 += (uint64_t)blockDim.x * TU) {
+      float xv[TU][8], pp[TU][2][8];
+      bool okv[TU];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) xv[k] = h == 0 ? __fadd_rn(xv[k], xp[k]) : __fadd_rn(xp[k], xv[k]);
-      }
-      // in-order combination: children below, x_v, children above
-      if (nd.self_pos == 0) {
+      for (int u = 0; u < TU; ++u) okv[u] = v0 + (uint64_t)u * blockDim.x < nv;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = xv[j];
-      } else {
-        load8_f32(mypart, e, acc);
-      }
-      for (int k = 1; k <= nd.nchild; ++k) {
-        if (k == nd.self_pos) {
+      for (int u = 0; u < TU; ++u) {
+        if (!okv[u]) continue;
+        const uint64_t e = e0 + (v0 + (uint64_t)u * blockDim.x) * 8;
+        load8<E>(mybuf, base + e, xv[u]);
+        if constexpr (PAIR) {
+          float xp[8];
+          load8<E>(pbuf, base + e, xp);
+          // node value x_v = fl32(x_2k + x_2k+1), lower rank first
 #pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], xv[j]);
-        } else {
-          load8_f32(mypart + (uint64_t)(k < nd.self_pos ? k : k - 1) * a.part_stride, e, t);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] = __fadd_rn(acc[j], t[j]);
+          for (int k = 0; k < 8; ++k) xv[u][k] = h == 0 ? __fadd_rn(xv[u][k], xp[k]) : __fadd_rn(xp[k], xv[u][k]);
         }
-      }
-      if (root) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = __fmul_rn(acc[j], a.scale);
-        store8<E>(mybuf, base + e, acc);
-        for (int k = 0; k < nd.nchild; ++k) store8<E>(a.buf[member(nd.child[k])], base + e, acc);
-        if constexpr (PAIR) store8<E>(pbuf, base + e, acc);
-      } else {
-        store8_f32(dst_part, e, acc);
+        for (int sl = 0; sl < 2; ++sl)
+          if (sl < nchild) load8_f32(mypart + (uint64_t)sl * a.part_stride, e, pp[u][sl]);
+      }
+#pragma unroll
+      for (int u = 0; u < TU; ++u) {
+        if (!okv[u]) continue;
+        const uint64_t e = e0 + (v0 + (uint64_t)u * blockDim.x) * 8;
+        // in-order combination: children below, x_v, children above (R10)
+        float acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = self_pos == 0 ? xv[u][j] : pp[u][0][j];
+#pragma unroll
+        for (int k = 1; k <= 2; ++k) {
+          if (k > nchild) break;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float t = k == self_pos ? xv[u][j] : (k < self_pos ? pp[u][k][j] : pp[u][k - 1][j]);
+            acc[j] = __fadd_rn(acc[j], t);
+          }
+        }
+        if (root) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] = __fmul_rn(acc[j], a.scale);
+          store8<E>(mybuf, base + e, acc);
+          for (int k = 0; k < nchild; ++k) store8<E>(a.buf[member(nd.child[k])], base + e, acc);
+          if constexpr (PAIR) store8<E>(pbuf, base + e, acc);
+        } else {
+          store8_f32(dst_part, e, acc);
+        }
       }
     }
     // ragged tail of the half (only the last chunk can have one)
@@ -590,10 +615,19 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     const int esz = (int)sizeof(typename E::T);
     const uint64_t b0 = (base + e0) * esz, b1 = (base + e1) * esz;  // byte range
     const uint64_t nv = (b1 - b0) / 16;
-    for (uint64_t v = threadIdx.x; v < nv; v += blockDim.x) {
-      const uint4 val = ld128(mybuf + b0 + v * 16);
-      for (int k = 0; k < nd.nchild; ++k) st128(a.buf[member(nd.child[k])] + b0 + v * 16, val);
-      if constexpr (PAIR) st128(a.buf[partner] + b0 + v * 16, val);
+    constexpr int DU = 4;  // 4 x 16 B loads in flight per thread before the stores
+    for (uint64_t v0 = threadIdx.x; v0 < nv; v0 += (uint64_t)blockDim.x * DU) {
+      uint4 val[DU];
+#pragma unroll
+      for (int u = 0; u < DU; ++u)
+        if (v0 + (uint64_t)u * blockDim.x < nv) val[u] = ld128(mybuf + b0 + (v0 + (uint64_t)u * blockDim.x) * 16);
+#pragma unroll
+      for (int u = 0; u < DU; ++u) {
+        if (v0 + (uint64_t)u * blockDim.x >= nv) break;
+        const uint64_t off = b0 + (v0 + (uint64_t)u * blockDim.x) * 16;
+        for (int k = 0; k < nd.nchild; ++k) st128(a.buf[member(nd.child[k])] + off, val[u]);
+        if constexpr (PAIR) st128(a.buf[partner] + off, val[u]);
+      }
     }
     for (uint64_t y = b0 + nv * 16 + threadIdx.x * esz; y < b1; y += (uint64_t)blockDim.x * esz) {
       if (esz == 2) {
@@ -629,6 +663,41 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
 // ---------------------------------------------------------------------------
 // Staging copy (buffers outside peer-mapped memory) and the device barrier.
 // ---------------------------------------------------------------------------
+// CE schedule's only SM work: fold the n copies of this rank's shard (its own
+// slice + the n-1 slices the copy engines pulled into staging) in rank order,
+// scale, cast, write the owner's result in place.  Local HBM traffic only.
+struct FoldArgs {
+  const char* src[kMaxRanks];  // rank-ordered sources
+  char* dst;
+  uint64_t count;
+  float scale;
+  int n;
+};
+
+template <class E>
+__global__ void __launch_bounds__(512) hfr_local_fold_kernel(const FoldArgs f) {
+  constexpr int K = E::kPerVec;
+  const uint64_t nvec = f.count / K;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    float acc[K], t[K];
+    E::widen(ld128(f.src[0] + i * 16), acc);
+    for (int r = 1; r < f.n; ++r) {
+      E::widen(ld128(f.src[r] + i * 16), t);
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc[k] = __fadd_rn(acc[k], t[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = __fmul_rn(acc[k], f.scale);
+    st128(f.dst + i * 16, E::narrow(acc));
+  }
+  for (uint64_t e = nvec * K + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < f.count; e += stride) {
+    float acc = E::load1(f.src[0], e);
+    for (int r = 1; r < f.n; ++r) acc = __fadd_rn(acc, E::load1(f.src[r], e));
+    E::store1(f.dst, e, __fmul_rn(acc, f.scale));
+  }
+}
+
 __global__ void __launch_bounds__(1024) hfr_copy_kernel(char* dst, const char* src, uint64_t bytes) {
   const uint64_t nv = bytes / 16;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;

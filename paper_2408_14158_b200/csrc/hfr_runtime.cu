@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -106,6 +107,12 @@ struct hfr_comm_s {
   int num_sms = 148;
   hfr_status_t sticky = HFR_SUCCESS;
   uint64_t launches = 0;
+  // CE schedule: helper streams (one per peer) so the copy engines run the
+  // n-1 pulls concurrently, fork/join events, and the host-side CE epoch
+  std::vector<cudaStream_t> helpers;
+  std::vector<cudaEvent_t> ce_events;
+  cudaEvent_t ce_fork = nullptr;
+  uint64_t ce_epoch = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -193,13 +200,16 @@ size_t dtype_size(hfr_dtype_t t) { return t == HFR_BFLOAT16 ? 2 : 4; }
 // larger message also runs FLAT (same result bits).
 int effective_algo(const hfr_comm_s* c, size_t bytes) {
   const int a = c->cfg.algo;
+  // CE needs separate processes (stream waits across ranks) and shards of at
+  // least 4096 elements; otherwise it runs FLAT (same bits)
+  if (a == HFR_ALGO_CE) return (c->virt || c->n == 1 || bytes < (size_t)c->n * 16384) ? HFR_ALGO_FLAT : HFR_ALGO_CE;
   if (a == HFR_ALGO_AUTO || a == HFR_ALGO_ONESHOT)
     return bytes <= c->cfg.oneshot_max_bytes ? HFR_ALGO_ONESHOT : HFR_ALGO_FLAT;
   return a;
 }
 
 hfr_status_t validate_cfg(const hfr_config_t& c) {
-  if (c.algo < HFR_ALGO_AUTO || c.algo > HFR_ALGO_ONESHOT) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.algo < HFR_ALGO_AUTO || c.algo > HFR_ALGO_CE) return HFR_ERR_INVALID_ARGUMENT;
   if (c.oneshot_max_bytes > (64u << 20)) return HFR_ERR_INVALID_ARGUMENT;
   if (c.chunk_elems % 256 != 0 || c.chunk_elems > (1u << 30)) return HFR_ERR_INVALID_ARGUMENT;
   if (c.max_ctas < 0 || c.max_ctas > kMaxCtas) return HFR_ERR_INVALID_ARGUMENT;
@@ -362,6 +372,17 @@ hfr_status_t common_init(hfr_comm_s* c) {
   HFR_CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   HFR_CU(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
   HFR_CU(cudaEventCreateWithFlags(&c->side_tail, cudaEventDisableTiming));
+  if (!c->virt && c->n > 1) {
+    for (int q = 0; q < c->n - 1; ++q) {
+      cudaStream_t h = nullptr;
+      cudaEvent_t ev = nullptr;
+      HFR_CU(cudaStreamCreateWithPriority(&h, cudaStreamNonBlocking, hi));
+      HFR_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      c->helpers.push_back(h);
+      c->ce_events.push_back(ev);
+    }
+    HFR_CU(cudaEventCreateWithFlags(&c->ce_fork, cudaEventDisableTiming));
+  }
   HFR_TRY(alloc_region(c, sizeof(Pad), &c->pad));
   HFR_TRY(alloc_region(c, c->cfg.scratch_bytes, &c->scratch));
   return HFR_SUCCESS;
@@ -373,7 +394,9 @@ hfr_status_t common_init(hfr_comm_s* c) {
 size_t inbox_bytes(const hfr_comm_s* c) { return round_up(2 * (size_t)c->n * c->cfg.oneshot_max_bytes, kAlign); }
 
 size_t scratch_need(const hfr_comm_s* c, size_t count, hfr_dtype_t dt, int algo) {
-  size_t need = inbox_bytes(c) + round_up(count * dtype_size(dt), kAlign);
+  size_t stage = round_up(count * dtype_size(dt), kAlign);
+  if (algo == HFR_ALGO_CE) stage = std::max(stage, (size_t)c->n * round_up((count / c->n + 256) * dtype_size(dt), kAlign));
+  size_t need = inbox_bytes(c) + stage;
   if (algo == HFR_ALGO_DBT) need += 2 * round_up(count, 64) * 4;
   if (algo == HFR_ALGO_PAIR_DBT) need += 2 * round_up(pair_half(count), 64) * 4;
   return need;
@@ -541,6 +564,122 @@ hfr_status_t run_oneshot(hfr_comm_s* c, char* const* local_bufs, uint64_t count,
   return launch(c, fn, g, threads, a, s);
 }
 
+// ---------------------------------------------------------------------------
+// CE schedule (copy engines + stream memory operations)
+// ---------------------------------------------------------------------------
+typedef int (*StreamValueFn)(cudaStream_t, unsigned long long, uint64_t, unsigned);
+constexpr unsigned kWaitGeq = 0x0;        // CU_STREAM_WAIT_VALUE_GEQ
+constexpr unsigned kWriteFenced = 0x0;    // CU_STREAM_WRITE_VALUE_DEFAULT: preceded by a system-wide fence
+
+hfr_status_t stream_value_fns(StreamValueFn* wr, StreamValueFn* wt) {
+  static StreamValueFn w = nullptr, t = nullptr;
+  if (!w || !t) {
+    cudaDriverEntryPointQueryResult q1, q2;
+    void *f1 = nullptr, *f2 = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &f1, cudaEnableDefault, &q1) != cudaSuccess ||
+        cudaGetDriverEntryPoint("cuStreamWaitValue64", &f2, cudaEnableDefault, &q2) != cudaSuccess ||
+        q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess)
+      return HFR_ERR_UNSUPPORTED;
+    w = (StreamValueFn)f1;
+    t = (StreamValueFn)f2;
+  }
+  *wr = w;
+  *wt = t;
+  return HFR_SUCCESS;
+}
+
+// Write `e` into field[rank] of every peer's pad (fenced), then make stream s
+// wait until field[q] >= e for every peer q.  No SM is involved.
+hfr_status_t ce_handshake(hfr_comm_s* c, cudaStream_t s, size_t field, uint64_t e) {
+  StreamValueFn wr = nullptr, wt = nullptr;
+  HFR_TRY(stream_value_fns(&wr, &wt));
+  for (int q = 0; q < c->n; ++q) {
+    if (q == c->rank) continue;
+    const unsigned long long dst = (unsigned long long)(c->pad.base[q] + field + 8 * (size_t)c->rank);
+    if (wr(s, dst, e, kWriteFenced) != 0) {
+      g_cuda_error = "cuStreamWriteValue64 on peer memory failed";
+      return HFR_ERR_CUDA;
+    }
+  }
+  for (int q = 0; q < c->n; ++q) {
+    if (q == c->rank) continue;
+    const unsigned long long src = (unsigned long long)(c->pad.base[c->rank] + field + 8 * (size_t)q);
+    if (wt(s, src, e, kWaitGeq) != 0) {
+      g_cuda_error = "cuStreamWaitValue64 failed";
+      return HFR_ERR_CUDA;
+    }
+  }
+  return HFR_SUCCESS;
+}
+
+// n-1 concurrent peer copies dst_q <- src_q (q != rank), one per helper stream
+hfr_status_t ce_pull(hfr_comm_s* c, cudaStream_t s, char* const* dst, char* const* src, const size_t* bytes) {
+  HFR_CU(cudaEventRecord(c->ce_fork, s));
+  int j = 0;
+  for (int q = 0; q < c->n; ++q) {
+    if (q == c->rank) continue;
+    HFR_CU(cudaStreamWaitEvent(c->helpers[j], c->ce_fork, 0));
+    if (bytes[q]) HFR_CU(cudaMemcpyAsync(dst[q], src[q], bytes[q], cudaMemcpyDeviceToDevice, c->helpers[j]));
+    HFR_CU(cudaEventRecord(c->ce_events[j], c->helpers[j]));
+    HFR_CU(cudaStreamWaitEvent(s, c->ce_events[j], 0));
+    ++j;
+  }
+  return HFR_SUCCESS;
+}
+
+hfr_status_t run_ce(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, cudaStream_t s) {
+  const int n = c->n, r = c->rank;
+  const size_t esz = dtype_size(dt);
+  uint64_t lo[kMaxRanks + 1];
+  for (int g = 0; g < n; ++g) lo[g] = count * g / n / 256 * 256;
+  lo[n] = count;
+  const size_t slot = round_up((count / n + 256) * esz, kAlign);
+  char* stage = stage_base(c, r);
+  const uint64_t e = ++c->ce_epoch;
+  // 1. every rank's buffer is ready ("wait for chunk-i transfer")
+  HFR_TRY(ce_handshake(c, s, offsetof(Pad, ce_ready), e));
+  // 2. reduce-scatter, transfer half: pull shard r of every peer (copy engines)
+  char* dst[kMaxRanks];
+  char* src[kMaxRanks];
+  size_t len[kMaxRanks];
+  for (int q = 0; q < n; ++q) {
+    dst[q] = stage + (size_t)q * slot;
+    src[q] = bufs[q] + lo[r] * esz;
+    len[q] = q == r ? 0 : (lo[r + 1] - lo[r]) * esz;
+  }
+  HFR_TRY(ce_pull(c, s, dst, src, len));
+  // 3. reduce-scatter, arithmetic half: rank-ordered fold of shard r (SMs, local)
+  FoldArgs f{};
+  for (int q = 0; q < n; ++q) f.src[q] = q == r ? bufs[r] + lo[r] * esz : dst[q];
+  f.dst = bufs[r] + lo[r] * esz;
+  f.count = lo[r + 1] - lo[r];
+  f.scale = c->cfg.scale;
+  f.n = n;
+  const int ctas = (int)std::max<uint64_t>(1, std::min<uint64_t>(c->cfg.max_ctas > 0 ? c->cfg.max_ctas : c->num_sms,
+                                                                  (f.count / 4 + 511) / 512));
+  if (dt == HFR_BFLOAT16)
+    hfr_local_fold_kernel<BF16><<<ctas, 512, 0, s>>>(f);
+  else
+    hfr_local_fold_kernel<F32><<<ctas, 512, 0, s>>>(f);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    note_cuda(err, "hfr_local_fold_kernel");
+    return HFR_ERR_CUDA;
+  }
+  ++c->launches;
+  // 4. every owner's result shard is final
+  HFR_TRY(ce_handshake(c, s, offsetof(Pad, ce_done), e));
+  // 5. all-gather: pull every peer's result shard into my buffer (copy engines)
+  for (int q = 0; q < n; ++q) {
+    dst[q] = bufs[r] + lo[q] * esz;
+    src[q] = bufs[q] + lo[q] * esz;
+    len[q] = q == r ? 0 : (lo[q + 1] - lo[q]) * esz;
+  }
+  HFR_TRY(ce_pull(c, s, dst, src, len));
+  // 6. every rank finished pulling from every buffer
+  return ce_handshake(c, s, offsetof(Pad, ce_exit), e);
+}
+
 hfr_status_t run_copy(hfr_comm_s* c, char* dst, const char* src, uint64_t bytes, cudaStream_t s) {
   if (bytes == 0) return HFR_SUCCESS;
   const int threads = 512;
@@ -650,7 +789,9 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     sig = fnv(sig, (uint64_t)zero_copy);
     sig = fnv(sig, algo == HFR_ALGO_FLAT ? 0 : c->cfg.chunk_elems);
     sig = fnv(sig, offset);
-    if (algo == HFR_ALGO_FLAT) {
+    if (algo == HFR_ALGO_CE && zero_copy) {
+      HFR_TRY(run_ce(c, bufs, count, dt, s));
+    } else if (algo == HFR_ALGO_FLAT || algo == HFR_ALGO_CE) {
       HFR_TRY(run_flat(c, bufs, count, dt, sig, s));
     } else {
       HFR_TRY(run_tree(c, bufs, count, dt, algo == HFR_ALGO_PAIR_DBT, sig, s));
@@ -870,6 +1011,9 @@ hfr_status_t hfr_finalize(hfr_comm_t c) {
     close_region(c, c->scratch);
     close_region(c, c->pad);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (cudaStream_t h : c->helpers) cudaStreamDestroy(h);
+    for (cudaEvent_t e : c->ce_events) cudaEventDestroy(e);
+    if (c->ce_fork) cudaEventDestroy(c->ce_fork);
     if (c->side_tail) cudaEventDestroy(c->side_tail);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->err_host) cudaFreeHost(c->err_host);

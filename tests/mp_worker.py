@@ -40,7 +40,7 @@ def gpu_cases(rank, world, port, outdir):
     try:
         comm = hfr.Comm.init(device=rank, config=hfr.Config(timeout_ms=8000, chunk_elems=512))
         for dtype in (gen.FP32, gen.BF16):
-            for algo in ("flat", "oneshot", "dbt", "pair_dbt", "auto"):
+            for algo in ("flat", "oneshot", "dbt", "pair_dbt", "auto", "ce"):
                 if algo == "pair_dbt" and world % 2:
                     continue
                 for N in (4096 + 13, 1_000_003):

@@ -118,9 +118,14 @@ def main():
                                                         map(int, a.ctas.split(",")), map(int, a.threads.split(","))):
             if algo == "pair_dbt" and n % 2:
                 continue
-            comm.set_config(hfr.Config(algo=algo, chunk_elems=chunk, max_ctas=ctas, threads=thr,
+            comm.set_config(hfr.Config(algo=algo if algo != "barrier" else "auto", chunk_elems=chunk, max_ctas=ctas, threads=thr,
                                        scale=1.0 / n, timeout_ms=30000))
-            fn = (lambda: comm.allreduce(views[0])) if multi else (lambda: comm.allreduce_virtual(views))
+            if algo == "barrier":   # handshake latency only (hfr_barrier kernel)
+                fn = lambda: comm.barrier(torch.cuda.current_stream())  # noqa: E731
+            elif multi:
+                fn = lambda: comm.allreduce(views[0])  # noqa: E731
+            else:
+                fn = lambda: comm.allreduce_virtual(views)  # noqa: E731
             t = timeit(fn, iters)
             st = comm.status()
             if st != hfr.SUCCESS:
