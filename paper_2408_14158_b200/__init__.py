@@ -35,7 +35,7 @@ EXPORTS = (
     "hfr_comm_local_ranks", "hfr_comm_rank", "hfr_comm_nranks", "hfr_mem_alloc", "hfr_mem_free",
     "hfr_register", "hfr_allreduce", "hfr_allreduce_virtual", "hfr_wait", "hfr_comm_status",
     "hfr_barrier", "hfr_finalize", "hfr_tree_query", "hfr_comm_launches", "hfr_status_string",
-    "hfr_last_cuda_error",
+    "hfr_last_cuda_error", "hfr_set_trace",
 )
 
 
@@ -106,6 +106,7 @@ def _lib():
             "hfr_comm_launches": (ctypes.c_uint64, [vp]),
             "hfr_status_string": (ctypes.c_char_p, [i]),
             "hfr_last_cuda_error": (ctypes.c_char_p, []),
+            "hfr_set_trace": (i, [vp, vp, sz]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -318,6 +319,15 @@ class Comm:
                                           ctypes.byref(req) if async_op else None)
         _check(st, "hfr_allreduce_virtual")
         return Work(self, req, list(tensors)) if async_op else None
+
+    def set_trace(self, buf=None):
+        """Diagnostic chunk timelines of the tree schedules into a uint8 CUDA
+        tensor (None: off).  See include/hfr.h hfr_set_trace."""
+        if buf is None:
+            _check(_lib().hfr_set_trace(self._h, None, 0), "hfr_set_trace")
+        else:
+            _check(_lib().hfr_set_trace(self._h, ctypes.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size()),
+                   "hfr_set_trace")
 
     def barrier(self, stream=None):
         _check(_lib().hfr_barrier(self._h, ctypes.c_void_p(_stream_handle(stream))), "hfr_barrier")

@@ -72,7 +72,31 @@ struct Args {
   int rank0;               // rank of blockIdx.y == 0
   int chunk;               // tree chunk elements (multiple of 256)
   int ntree;               // nodes per tree (n, or n/2 for PAIR)
+  uint32_t trace_cap;      // diagnostic trace: events per CTA (0 = off)
+  uint64_t* trace;         // [local rank][CTA][trace_cap][4] u64, see Tracer
   TreeNode tree[2][kMaxRanks];
+};
+
+// Diagnostic per-CTA event log (hfr_set_trace): thread 0 records
+// {tag, t_wait_start, t_work_start, t_done} in globaltimer ns.
+struct Tracer {
+  uint64_t* p = nullptr;
+  uint32_t cap = 0, n = 0;
+  __device__ explicit Tracer(const Args& a) {
+    if (a.trace && threadIdx.x == 0) {
+      cap = a.trace_cap;
+      p = a.trace + ((uint64_t)blockIdx.y * kMaxCtas + blockIdx.x) * cap * 4;
+    }
+  }
+  __device__ __forceinline__ void rec(uint64_t tag, uint64_t t0, uint64_t t1, uint64_t t2) {
+    if (p && n < cap) {
+      p[4 * n] = tag;
+      p[4 * n + 1] = t0;
+      p[4 * n + 2] = t1;
+      p[4 * n + 3] = t2;
+      ++n;
+    }
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -502,13 +526,16 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
   const float* const mypart = a.part[rank];
   auto member = [&](int node) { return PAIR ? 2 * node + h : node; };
 
+  Tracer tr(a);
   // ---- up pass -----------------------------------------------------------
   for (uint64_t c = a.c_lo + b; c < c_end; c += gridDim.x) {
     const TreeNode nd = a.tree[c & 1][me];
     const uint32_t lc = (uint32_t)(c - a.c_lo);
+    const uint64_t tw = tr.p ? globaltimer() : 0;
     bool got = true;
     if (threadIdx.x < nd.nchild) got = wait_ge(a, &mypad->up[threadIdx.x][lc], ep);
     if (!__syncthreads_and(got)) return;
+    const uint64_t tk = tr.p ? globaltimer() : 0;
 
     const uint64_t e0 = c * C, e1 = (e0 + C < len) ? e0 + C : len;  // offsets within the half
     const uint64_t nv = (e1 - e0) / 8;
@@ -599,6 +626,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
       } else {
         st_relaxed_sys(&a.pad[member(nd.parent)]->up[nd.slot][lc], ep);
       }
+      tr.rec((1ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, globaltimer());
     }
   }
 
@@ -607,10 +635,15 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     const TreeNode nd = a.tree[c & 1][me];
     if (nd.parent < 0) continue;  // the root already pushed its final chunk
     const uint32_t lc = (uint32_t)(c - a.c_lo);
+    const uint64_t tw = tr.p ? globaltimer() : 0;
     bool got = true;
     if (threadIdx.x == 0) got = wait_ge(a, &mypad->down[lc], ep);
     if (!__syncthreads_and(got)) return;
-    if (nd.nchild == 0 && !PAIR) continue;
+    const uint64_t tk = tr.p ? globaltimer() : 0;
+    if (nd.nchild == 0 && !PAIR) {
+      tr.rec((2ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, tk);
+      continue;
+    }
     const uint64_t e0 = c * C, e1 = (e0 + C < len) ? e0 + C : len;
     const int esz = (int)sizeof(typename E::T);
     const uint64_t b0 = (base + e0) * esz, b1 = (base + e1) * esz;  // byte range
@@ -645,6 +678,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
       fence_acq_rel_sys();
       for (int k = 0; k < nd.nchild; ++k) st_relaxed_sys(&a.pad[member(nd.child[k])]->down[lc], ep);
       if constexpr (PAIR) st_relaxed_sys(&a.pad[partner]->pdown[lc], ep);
+      tr.rec((2ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, globaltimer());
     }
   }
 
@@ -654,7 +688,12 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     const uint64_t onch = (olen + C - 1) / C;
     const uint64_t oend = onch < a.c_hi ? onch : a.c_hi;
     for (uint64_t c = a.c_lo + b; c < oend; c += gridDim.x) {
-      if (threadIdx.x == 0) wait_ge(a, &mypad->pdown[(uint32_t)(c - a.c_lo)], ep);
+      if (threadIdx.x == 0) {
+        const uint64_t tw = tr.p ? globaltimer() : 0;
+        wait_ge(a, &mypad->pdown[(uint32_t)(c - a.c_lo)], ep);
+        const uint64_t tk = tr.p ? globaltimer() : 0;
+        tr.rec((3ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, tk);
+      }
     }
   }
   end_epoch(mypad, ep);

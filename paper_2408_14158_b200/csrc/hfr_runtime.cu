@@ -113,6 +113,8 @@ struct hfr_comm_s {
   std::vector<cudaEvent_t> ce_events;
   cudaEvent_t ce_fork = nullptr;
   uint64_t ce_epoch = 0;
+  uint64_t* trace = nullptr;  // hfr_set_trace (diagnostic)
+  uint32_t trace_cap = 0;
 };
 
 // ---------------------------------------------------------------------------
@@ -484,6 +486,8 @@ void base_args(hfr_comm_s* c, Args& a, uint64_t count, uint64_t sig) {
   a.scale = c->cfg.scale;
   a.n = c->n;
   a.rank0 = c->virt ? 0 : c->rank;
+  a.trace = c->trace;
+  a.trace_cap = c->trace_cap;
 }
 
 hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
@@ -1033,6 +1037,19 @@ hfr_status_t hfr_tree_query(int n, int which, int* parent, int* child0, int* chi
     child0[v] = ch[v][0];
     child1[v] = ch[v][1];
   }
+  return HFR_SUCCESS;
+}
+
+hfr_status_t hfr_set_trace(hfr_comm_t c, void* dev_buf, size_t bytes) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  const size_t per = (size_t)32 * kMaxCtas * c->local;
+  if (!dev_buf || bytes < per) {
+    c->trace = nullptr;
+    c->trace_cap = 0;
+    return dev_buf ? HFR_ERR_INVALID_ARGUMENT : HFR_SUCCESS;
+  }
+  c->trace = (uint64_t*)dev_buf;
+  c->trace_cap = (uint32_t)std::min<size_t>(bytes / per, 1u << 20);
   return HFR_SUCCESS;
 }
 
