@@ -90,7 +90,7 @@ typedef int (*hfr_allgather_fn)(const void* send, void* recv, size_t bytes, void
 typedef struct {
     int algo;             /* hfr_algo_t */
     size_t chunk_elems;   /* tree chunk size in elements (Alg. 1 "Chunk_Size");
-                             multiple of 256; 0 -> 8192.  Changes DBT/PAIR_DBT bits (reading R8),
+                             multiple of 256; 0 -> 32768.  Changes DBT/PAIR_DBT bits (reading R8),
                              never FLAT's. */
     int max_ctas;         /* CTAs per rank; 0 -> one per SM.  Caps the SMs the comm uses. */
     int threads;          /* threads per CTA (128..512, multiple of 32); 0 -> 512 */

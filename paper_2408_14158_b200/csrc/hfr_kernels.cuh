@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     // TU units of 8 elements per thread per iteration: every load of the TU
     // units (x_v, the partner's x, the children's partials) is issued before
     // the first add, so a CTA keeps TU x (2..4) x 32 B per thread in flight.
-    constexpr int TU = 2;
+    constexpr int TU = 1;
     const int nchild = nd.nchild, self_pos = nd.self_pos;
     for (uint64_t v0 = threadIdx.x; v0 < nv; v0 += (uint64_t)blockDim.x * TU) {
       float xv[TU][8], pp[TU][2][8];

@@ -222,7 +222,7 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
 }
 
 void resolve_defaults(hfr_config_t& c) {
-  if (c.chunk_elems == 0) c.chunk_elems = 8192;
+  if (c.chunk_elems == 0) c.chunk_elems = 32768;
   if (c.threads == 0) c.threads = 512;
   if (c.scratch_bytes == 0) c.scratch_bytes = 256ull << 20;
   if (c.timeout_ms == 0) c.timeout_ms = 60000;

@@ -1,11 +1,15 @@
 // p2p_probe.cu — NVLink microbenchmark (one process, n GPUs, peer access):
 // what per-direction bandwidth do SM-driven remote loads, remote stores and
-// their mix reach on this box?  Used to choose the transfer style of the
+// their mix reach on this box, and what does a per-chunk system fence (the
+// tree schedule's handoff) cost?  Used to choose the transfer style of the
 // HFReduce kernels.  No cross-GPU waits: every kernel only
 // moves data, so concurrent launches on several GPUs are safe.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o p2p_probe tools/p2p_probe.cu
-//   ./p2p_probe <ngpus> <MiB per peer> <ctas> <threads>
+//   ./p2p_probe <ngpus> <MiB per peer> <ctas> <threads> [fence_chunk_KiB]
+//
+// Every thread interleaves all peers (vector i of every peer segment before
+// vector i+stride), so no GPU is a hotspot.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -13,9 +17,9 @@
 
 #define CK(x)                                                                         \
   do {                                                                                \
-    cudaError_t e = (x);                                                              \
-    if (e != cudaSuccess) {                                                           \
-      fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e)); \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess) {                                                          \
+      fprintf(stderr, "%s:%d %s: %s\n", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
       exit(1);                                                                        \
     }                                                                                 \
   } while (0)
@@ -23,25 +27,49 @@
 struct Ptrs {
   const uint4* src[16];
   uint4* dst[16];
+  unsigned long long* flag;  // per-chunk handoff target (fence mode)
   int n;
 };
 
-// each CTA grid-strides over all peers' segments: vector i of segment p
-// copies src[p][i] -> dst[p][i]
+// vector i of every segment k (k-inner), U vectors in flight per segment
 template <int U>
 __global__ void __launch_bounds__(512) move(Ptrs p, uint64_t nvec) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (int k = 0; k < p.n; ++k) {
-    const uint4* s = p.src[k];
-    uint4* d = p.dst[k];
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += U * stride) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += U * stride) {
+    for (int k = 0; k < p.n; ++k) {
       uint4 v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (i + u * stride < nvec) v[u] = s[i + u * stride];
+        if (i + u * stride < nvec) v[u] = p.src[k][i + u * stride];
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (i + u * stride < nvec) d[i + u * stride] = v[u];
+        if (i + u * stride < nvec) p.dst[k][i + u * stride] = v[u];
+    }
+  }
+}
+
+// chunked: CTA b moves contiguous chunks of `cvec` vectors of every segment;
+// after each chunk: __syncthreads, thread 0 fence.acq_rel.sys + flag store
+// (exactly the tree kernel's per-chunk handoff).
+__global__ void __launch_bounds__(512) move_fenced(Ptrs p, uint64_t nvec, uint64_t cvec) {
+  const uint64_t nchunks = (nvec + cvec - 1) / cvec;
+  for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    const uint64_t lo = c * cvec, hi = lo + cvec < nvec ? lo + cvec : nvec;
+    for (int k = 0; k < p.n; ++k) {
+      for (uint64_t i = lo + threadIdx.x; i < hi; i += 4 * blockDim.x) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i + u * blockDim.x < hi) v[u] = p.src[k][i + u * blockDim.x];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i + u * blockDim.x < hi) p.dst[k][i + u * blockDim.x] = v[u];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p.flag + blockIdx.x), "l"((unsigned long long)c) : "memory");
     }
   }
 }
@@ -51,9 +79,11 @@ int main(int argc, char** argv) {
   const size_t mib = argc > 2 ? atol(argv[2]) : 64;
   const int ctas = argc > 3 ? atoi(argv[3]) : 148;
   const int threads = argc > 4 ? atoi(argv[4]) : 512;
+  const size_t fence_kib = argc > 5 ? atol(argv[5]) : 0;
   const size_t bytes = mib << 20;
   const uint64_t nvec = bytes / 16;
   uint4 *local[8], *inbox[8];  // inbox[g] holds n slots of `bytes` (one per peer)
+  unsigned long long* flags[8];
   cudaStream_t st[8];
   cudaEvent_t e0[8], e1[8];
   for (int g = 0; g < n; ++g) {
@@ -66,6 +96,7 @@ int main(int argc, char** argv) {
       }
     CK(cudaMalloc(&local[g], bytes * n));
     CK(cudaMalloc(&inbox[g], bytes * n));
+    CK(cudaMalloc(&flags[g], 8 * 4096));
     CK(cudaMemset(local[g], 1, bytes * n));
     CK(cudaMemset(inbox[g], 2, bytes * n));
     CK(cudaStreamCreateWithFlags(&st[g], cudaStreamNonBlocking));
@@ -75,29 +106,35 @@ int main(int argc, char** argv) {
   const char* names[] = {"read  (pull from peers)", "write (push to peers)", "mixed (pull half, push half)",
                          "read  one-way (GPU0 only)", "write one-way (GPU0 only)"};
   for (int mode = 0; mode < 5; ++mode) {
+    if (fence_kib && mode != 1) continue;
     for (int rep = 0; rep < 3; ++rep) {
       for (int g = 0; g < n; ++g) {
         if (mode >= 3 && g != 0) continue;
         CK(cudaSetDevice(g));
         Ptrs p{};
         p.n = 0;
+        p.flag = flags[(g + 1) % n];
         uint64_t per = nvec;
         for (int h = 0; h < n; ++h) {
           if (h == g) continue;
           uint4* peer_slot = inbox[h] + (size_t)g * nvec;
           uint4* my_slot = local[g] + (size_t)h * nvec;
-          if (mode == 0 || mode == 3) {  // pull: read peer, write local
+          if (mode == 0 || mode == 3) {
             p.src[p.n] = peer_slot; p.dst[p.n++] = my_slot;
-          } else if (mode == 1 || mode == 4) {  // push: read local, write peer
+          } else if (mode == 1 || mode == 4) {
             p.src[p.n] = my_slot; p.dst[p.n++] = peer_slot;
-          } else {  // mixed: pull the first half, push the second half
+          } else {
             per = nvec / 2;
             p.src[p.n] = peer_slot; p.dst[p.n++] = my_slot;
             p.src[p.n] = my_slot + per; p.dst[p.n++] = peer_slot + per;
           }
         }
         CK(cudaEventRecord(e0[g], st[g]));
-        move<4><<<ctas, threads, 0, st[g]>>>(p, per);
+        if (fence_kib)
+          move_fenced<<<ctas, threads, 0, st[g]>>>(p, per, (fence_kib << 10) / 16 / p.n);
+        else
+          move<4><<<ctas, threads, 0, st[g]>>>(p, per);
+        CK(cudaGetLastError());
         CK(cudaEventRecord(e1[g], st[g]));
       }
       float worst = 0;
@@ -109,11 +146,10 @@ int main(int argc, char** argv) {
         CK(cudaEventElapsedTime(&ms, e0[g], e1[g]));
         if (ms > worst) worst = ms;
       }
-      // bytes entering one GPU over NVLink (== leaving, by symmetry)
       const double per_dir = (double)bytes * (n - 1);
       if (rep == 2)
-        printf("n=%d %-30s %5zu MiB/peer ctas=%3d thr=%d: %8.3f ms -> %6.1f GB/s per GPU per direction\n", n,
-               names[mode], mib, ctas, threads, worst, per_dir / worst / 1e6);
+        printf("n=%d %-30s %5zu MiB/peer ctas=%3d thr=%d fence_chunk=%zuKiB: %8.3f ms -> %6.1f GB/s per GPU per direction\n",
+               n, names[mode], mib, ctas, threads, fence_kib, worst, per_dir / worst / 1e6);
     }
   }
   return 0;
