@@ -99,6 +99,10 @@ typedef struct {
     int timeout_ms;       /* cross-rank spin-wait timeout; 0 -> 60000 */
     size_t oneshot_max_bytes; /* largest message for ONESHOT (and AUTO's switch point); fixed at
                                  init (sizes the per-rank inbox: 2 * nranks * this); 0 -> 512 KiB */
+    int stream_gate;      /* 1: before launching an SM schedule, make the stream wait (stream memory
+                             operations in the copy-engine front end, no SM) until every rank has
+                             reached this call, so no CTA spins on a late peer (overlap with compute);
+                             real comms only.  0 (default): off. */
 } hfr_config_t;
 
 /* Fill *cfg with the defaults above (algo AUTO, scale 1.0). */

@@ -19,7 +19,9 @@ from dataclasses import dataclass
 from typing import Optional, Sequence
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libhfr.so")
+# HFR_LIB selects an experimental in-tree build (e.g. libhfr_hints.so); the
+# default is the production libhfr.so.  Either way a missing file raises.
+LIB_PATH = os.environ.get("HFR_LIB") or os.path.join(_PKG, "libhfr.so")
 
 SUCCESS, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED, ERR_CUDA, ERR_OUT_OF_MEMORY, ERR_PROTOCOL, \
     ERR_TIMEOUT, ERR_NOT_INITIALIZED, ERR_INTERNAL = range(9)
@@ -51,7 +53,7 @@ class HfrError(RuntimeError):
 class _Config(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int), ("chunk_elems", ctypes.c_size_t), ("max_ctas", ctypes.c_int),
                 ("threads", ctypes.c_int), ("scale", ctypes.c_float), ("scratch_bytes", ctypes.c_size_t),
-                ("timeout_ms", ctypes.c_int), ("oneshot_max_bytes", ctypes.c_size_t)]
+                ("timeout_ms", ctypes.c_int), ("oneshot_max_bytes", ctypes.c_size_t), ("stream_gate", ctypes.c_int)]
 
 
 @dataclass
@@ -65,12 +67,13 @@ class Config:
     scratch_bytes: int = 0
     timeout_ms: int = 0
     oneshot_max_bytes: int = 0
+    stream_gate: int = 0
 
     def _c(self) -> _Config:
         if self.algo not in ALGOS:
             raise ValueError(f"unknown algo {self.algo!r}")
         return _Config(ALGOS[self.algo], self.chunk_elems, self.max_ctas, self.threads, self.scale,
-                       self.scratch_bytes, self.timeout_ms, self.oneshot_max_bytes)
+                       self.scratch_bytes, self.timeout_ms, self.oneshot_max_bytes, self.stream_gate)
 
 
 _LIB = None

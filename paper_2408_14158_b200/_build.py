@@ -24,10 +24,14 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if force or stale():
-        tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [NVCC, *FLAGS, "-o", tmp, *SRC]
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+    """Build libhfr.so (or an experimental variant, e.g. variant="hints" ->
+    libhfr_hints.so with -DHFR_STREAM_HINTS=1, loaded via HFR_LIB)."""
+    lib = LIB if not variant else LIB.replace("libhfr.so", f"libhfr_{variant}.so")
+    defs = {"hints": ["-DHFR_STREAM_HINTS=1"]}.get(variant, [])
+    if force or variant or stale():
+        tmp = lib + f".tmp{os.getpid()}"
+        cmd = [NVCC, *FLAGS, *defs, "-o", tmp, *SRC]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -36,10 +40,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc failed building libhfr.so")
         if verbose:
             sys.stderr.write(r.stderr)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    variant = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--variant=")), "")
+    print(build(force=True, verbose="-v" in sys.argv, variant=variant))

@@ -218,6 +218,7 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
   if (c.threads != 0 && (c.threads < 128 || c.threads > 512 || c.threads % 32 != 0)) return HFR_ERR_INVALID_ARGUMENT;
   if (!(c.scale == c.scale)) return HFR_ERR_INVALID_ARGUMENT;
   if (c.timeout_ms < 0) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.stream_gate != 0 && c.stream_gate != 1) return HFR_ERR_INVALID_ARGUMENT;
   return HFR_SUCCESS;
 }
 
@@ -372,7 +373,8 @@ hfr_status_t common_init(hfr_comm_s* c) {
   HFR_CU(cudaHostGetDevicePointer((void**)&c->err_dev, c->err_host, 0));
   int lo = 0, hi = 0;
   HFR_CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  HFR_CU(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+  const char* prio = getenv("HFR_SIDE_PRIORITY");  // experiment knob: "low" = lowest priority
+  HFR_CU(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio && !strcmp(prio, "low") ? lo : hi));
   HFR_CU(cudaEventCreateWithFlags(&c->side_tail, cudaEventDisableTiming));
   if (!c->virt && c->n > 1) {
     for (int q = 0; q < c->n - 1; ++q) {
@@ -774,6 +776,8 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     uint32_t sbits;
     memcpy(&sbits, &c->cfg.scale, 4);
     sig = fnv(sig, sbits);
+    const bool gate = c->cfg.stream_gate && !c->virt && c->n > 1 && algo != HFR_ALGO_CE && !capturing;
+    if (gate) HFR_TRY(ce_handshake(c, s, offsetof(Pad, ce_ready), ++c->ce_epoch));
     if (algo == HFR_ALGO_ONESHOT) {
       // peers never touch this rank's buffer: no staging, any device pointer
       HFR_TRY(run_oneshot(c, local_bufs, count, dt, sig, s));

@@ -55,6 +55,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--algo", default="flat")
     ap.add_argument("--layers", type=int, default=LAYERS, help="fewer layers for a quick run")
+    ap.add_argument("--gate", type=int, default=0, help="hfr_config.stream_gate")
     a = ap.parse_args()
 
     import torch
@@ -77,7 +78,8 @@ def main():
         params = [p for p in params if not p[0].startswith("l") or p[0][:p[0].index(".") + 1] in keep
                   or p[0].startswith("lm_head")]
     numels = [o * i for _, o, i in params]
-    comm = hfr.Comm.init(device=local, config=hfr.Config(algo=a.algo, max_ctas=a.max_ctas, scale=1.0 / world))
+    comm = hfr.Comm.init(device=local, config=hfr.Config(algo=a.algo, max_ctas=a.max_ctas, scale=1.0 / world,
+                                                        stream_gate=a.gate))
     ddp = HaiScaleDDP(comm, numels, torch.bfloat16, bucket_bytes=a.bucket_mib << 20)
     T = a.tokens
     g = torch.Generator(device=dev).manual_seed(3000 + rank)
@@ -136,6 +138,7 @@ def main():
         print(json.dumps({
             "config": "C5 HaiScale DDP", "n": n, "params": ddp.total, "grad_bytes": S,
             "buckets": len(ddp.bucket_ranges), "bucket_mib": a.bucket_mib, "max_ctas": a.max_ctas, "algo": a.algo,
+            "stream_gate": a.gate, "side_priority": os.environ.get("HFR_SIDE_PRIORITY", "high"),
             "tokens": T, "T_bwd_ms": tb * 1e3, "T_comm_ms": tc * 1e3, "T_both_ms": tt * 1e3,
             "overlap": (tb + tc - tt) / tc, "bwd_slowdown": tt / tb,
             "comm_busbw": S / tc * 2 * (n - 1) / n / 1e9, "bwd_tflops": flops / tb / 1e12,
