@@ -81,14 +81,15 @@ class Clocks:
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, interval_ms: int = 100):
         self.device = device
+        self.interval_ms = interval_ms
         self.p = None
 
     def start(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                       "-i", str(self.device), "-lms", "100"],
+                                       "-i", str(self.device), "-lms", str(self.interval_ms)],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.p = None
@@ -361,7 +362,7 @@ def main():
                 "hfr_over_nccl": value / busbw(S, tn, n) if tn > 0 else None}
         del t
     variants = {}
-    if not args.no_variants:
+    if multi and not args.no_variants:  # tree schedules over NVLink (virtual-rank trees are not meaningful)
         for algo in ("dbt", "pair_dbt"):
             if algo == args.algo or (algo == "pair_dbt" and n % 2):
                 continue

@@ -25,10 +25,10 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
-    """Build libhfr.so (or an experimental variant, e.g. variant="hints" ->
-    libhfr_hints.so with -DHFR_STREAM_HINTS=1, loaded via HFR_LIB)."""
+    """Build libhfr.so, or an experimental variant libhfr_<variant>.so with
+    -DHFR_VARIANT_<VARIANT>=1 (selected at run time with HFR_LIB=<path>)."""
     lib = LIB if not variant else LIB.replace("libhfr.so", f"libhfr_{variant}.so")
-    defs = {"hints": ["-DHFR_STREAM_HINTS=1"]}.get(variant, [])
+    defs = [f"-DHFR_VARIANT_{variant.upper()}=1"] if variant else []
     if force or variant or stale():
         tmp = lib + f".tmp{os.getpid()}"
         cmd = [NVCC, *FLAGS, *defs, "-o", tmp, *SRC]

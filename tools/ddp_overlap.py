@@ -123,11 +123,15 @@ def main():
 
     backward(True)  # warm-up (cuBLAS heuristics, IPC mappings)
     comm_only()
+    from bench import Clocks
     res = {"bwd": [], "comm": [], "both": []}
-    for _ in range(a.reps):
-        res["bwd"].append(timed(lambda: backward(False)))
-        res["comm"].append(timed(comm_only))
-        res["both"].append(timed(lambda: backward(True)))
+    clk = {}
+    for name, fn in (("bwd", lambda: backward(False)), ("comm", comm_only), ("both", lambda: backward(True))):
+        ck = Clocks(local, interval_ms=20)
+        ck.start()
+        for _ in range(a.reps):
+            res[name].append(timed(fn))
+        clk[name] = ck.stop()
     if comm.status() != hfr.SUCCESS:
         raise SystemExit(hfr.status_string(comm.status()))
     tb, tc, tt = (statistics.median(res[k]) for k in ("bwd", "comm", "both"))
@@ -142,7 +146,7 @@ def main():
             "tokens": T, "T_bwd_ms": tb * 1e3, "T_comm_ms": tc * 1e3, "T_both_ms": tt * 1e3,
             "overlap": (tb + tc - tt) / tc, "bwd_slowdown": tt / tb,
             "comm_busbw": S / tc * 2 * (n - 1) / n / 1e9, "bwd_tflops": flops / tb / 1e12,
-            "reps": res}), flush=True)
+            "clocks": clk, "reps": res}), flush=True)
     comm.finalize()
     dist.destroy_process_group()
 
