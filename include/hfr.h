@@ -71,14 +71,23 @@ typedef enum {
  *            and only a short local fold kernel runs on the SMs — for
  *            overlapping with compute (DDP).  Same result bits as FLAT.
  *            Needs peer-mapped buffers on a real comm; otherwise runs FLAT.
- *   AUTO     ONESHOT up to oneshot_max_bytes, FLAT above. */
+ *   NVLS     ORDER-RELAXED NVLink SHARP path: the NVSwitch sums
+ *            the n copies (multimem.ld_reduce) and multicasts the owner's
+ *            scaled result (multimem.st).  The switch chooses the summation
+ *            order, so results are NOT bit-exact: they are held to DESIGN.md
+ *            reading R18 (fp32 |err| <= 1e-6 * sum|x|, bf16 <= 1 ulp + that).
+ *            Needs hfr_config.nvls_bytes > 0 at init and a buffer from
+ *            hfr_mem_alloc inside that arena; otherwise UNSUPPORTED (never a
+ *            silent change of numerics).
+ *   AUTO     ONESHOT up to oneshot_max_bytes, FLAT above (never NVLS). */
 typedef enum {
     HFR_ALGO_AUTO = 0,
     HFR_ALGO_FLAT = 1,
     HFR_ALGO_DBT = 2,
     HFR_ALGO_PAIR_DBT = 3,
     HFR_ALGO_ONESHOT = 4,
-    HFR_ALGO_CE = 5
+    HFR_ALGO_CE = 5,
+    HFR_ALGO_NVLS = 6
 } hfr_algo_t;
 
 /* All-gather callback used ONLY by the collective setup calls (hfr_init,
@@ -103,6 +112,11 @@ typedef struct {
                              operations in the copy-engine front end, no SM) until every rank has
                              reached this call, so no CTA spins on a late peer (overlap with compute);
                              real comms only.  0 (default): off. */
+    size_t nvls_bytes;    /* > 0: at init, build an NVLS multicast arena of this many bytes per rank
+                             (cuMulticast*, fixed at init); hfr_mem_alloc then hands out memory from
+                             it (usable by every algo; required by NVLS).  Ignored for virtual comms.
+                             If the box has no NVLS, init still succeeds and NVLS calls return
+                             UNSUPPORTED.  0 (default): no arena. */
 } hfr_config_t;
 
 /* Fill *cfg with the defaults above (algo AUTO, scale 1.0). */

@@ -25,9 +25,9 @@ LIB_PATH = os.environ.get("HFR_LIB") or os.path.join(_PKG, "libhfr.so")
 
 SUCCESS, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED, ERR_CUDA, ERR_OUT_OF_MEMORY, ERR_PROTOCOL, \
     ERR_TIMEOUT, ERR_NOT_INITIALIZED, ERR_INTERNAL = range(9)
-ALGO_AUTO, ALGO_FLAT, ALGO_DBT, ALGO_PAIR_DBT, ALGO_ONESHOT, ALGO_CE = range(6)
+ALGO_AUTO, ALGO_FLAT, ALGO_DBT, ALGO_PAIR_DBT, ALGO_ONESHOT, ALGO_CE, ALGO_NVLS = range(7)
 ALGOS = {"auto": ALGO_AUTO, "flat": ALGO_FLAT, "dbt": ALGO_DBT, "pair_dbt": ALGO_PAIR_DBT, "oneshot": ALGO_ONESHOT,
-         "ce": ALGO_CE}
+         "ce": ALGO_CE, "nvls": ALGO_NVLS}
 FLOAT32, BFLOAT16 = 0, 1
 SUM = 0
 
@@ -53,7 +53,8 @@ class HfrError(RuntimeError):
 class _Config(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int), ("chunk_elems", ctypes.c_size_t), ("max_ctas", ctypes.c_int),
                 ("threads", ctypes.c_int), ("scale", ctypes.c_float), ("scratch_bytes", ctypes.c_size_t),
-                ("timeout_ms", ctypes.c_int), ("oneshot_max_bytes", ctypes.c_size_t), ("stream_gate", ctypes.c_int)]
+                ("timeout_ms", ctypes.c_int), ("oneshot_max_bytes", ctypes.c_size_t), ("stream_gate", ctypes.c_int),
+                ("nvls_bytes", ctypes.c_size_t)]
 
 
 @dataclass
@@ -68,12 +69,14 @@ class Config:
     timeout_ms: int = 0
     oneshot_max_bytes: int = 0
     stream_gate: int = 0
+    nvls_bytes: int = 0
 
     def _c(self) -> _Config:
         if self.algo not in ALGOS:
             raise ValueError(f"unknown algo {self.algo!r}")
         return _Config(ALGOS[self.algo], self.chunk_elems, self.max_ctas, self.threads, self.scale,
-                       self.scratch_bytes, self.timeout_ms, self.oneshot_max_bytes, self.stream_gate)
+                       self.scratch_bytes, self.timeout_ms, self.oneshot_max_bytes, self.stream_gate,
+                       self.nvls_bytes)
 
 
 _LIB = None

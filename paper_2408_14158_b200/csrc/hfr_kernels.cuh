@@ -37,6 +37,7 @@ struct Pad {
   uint64_t ce_ready[kMaxRanks]; // CE schedule: rank q's buffer is ready (stream memop flags)
   uint64_t ce_done[kMaxRanks];  //   rank q's result shard is final
   uint64_t ce_exit[kMaxRanks];  //   rank q finished pulling from every peer
+  uint32_t nvls_seq[kMaxCtas]; // NVLS launches seen by CTA b (local only)
   uint64_t launch_epoch;        // epoch of the last completed launch on this rank
   uint32_t done_ctas;           // CTAs of the current launch that have finished
 };
@@ -72,6 +73,9 @@ struct Args {
   int rank0;               // rank of blockIdx.y == 0
   int chunk;               // tree chunk elements (multiple of 256)
   int ntree;               // nodes per tree (n, or n/2 for PAIR)
+  char* mcbuf;              // NVLS: multicast VA of this call's buffer
+  uint32_t* mc_exit;       // NVLS: multicast VA of the exit counters [kMaxCtas]
+  uint32_t* uc_exit;       // NVLS: local unicast VA of the same counters
   uint32_t trace_cap;      // diagnostic trace: events per CTA (0 = off)
   uint64_t* trace;         // [local rank][CTA][trace_cap][4] u64, see Tracer
   TreeNode tree[2][kMaxRanks];
@@ -460,6 +464,103 @@ __global__ void __launch_bounds__(512) hfr_oneshot_kernel(const Args a) {
     E::store1(dst, e, __fmul_rn(acc, a.scale));
   }
   end_epoch(a.pad[rank], ep);
+}
+
+// ---------------------------------------------------------------------------
+// NVLS (order-relaxed; hfr_nvls.cuh): the NVSwitch reduces and multicasts.
+//
+// Rank g owns shard g.  Per 16 B: one multimem.ld_reduce on the multicast
+// address returns the sum over all n GPUs (fp32; bf16 accumulated in fp32 by
+// the switch and rounded once), the owner multiplies by scale, and one
+// multimem.st writes the result into all n GPUs' buffers.  The switch picks
+// the summation order, so the bits are NOT the rank-ascending fold's: the
+// result is held to reading R18's bound.  Entry: the usual packed-flag
+// handshake (argument check); exit: one multimem.red.release per CTA bumps
+// counter b on every GPU, each CTA waits until all n ranks' CTA b arrived.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void nvls_vec_f32(char* mc, float scale) {
+  float x, y, z, w;
+  asm volatile("multimem.ld_reduce.weak.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(x), "=f"(y), "=f"(z), "=f"(w)
+               : "l"(mc)
+               : "memory");
+  x = __fmul_rn(x, scale);
+  y = __fmul_rn(y, scale);
+  z = __fmul_rn(z, scale);
+  w = __fmul_rn(w, scale);
+  asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "f"(x), "f"(y), "f"(z), "f"(w)
+               : "memory");
+}
+
+__device__ __forceinline__ void nvls_vec_bf16(char* mc, float scale) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.weak.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(mc)
+               : "memory");
+  if (scale != 1.0f) {
+    float f[8];
+    BF16::widen(v, f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(f[k], scale);
+    v = BF16::narrow(f);
+  }
+  asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "f"(__uint_as_float(v.x)),
+               "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
+               : "memory");
+}
+
+template <class E>
+__global__ void __launch_bounds__(512) hfr_nvls_kernel(const Args a) {
+  const int rank = a.rank0;  // real comms only
+  const int n = a.n;
+  const int b = blockIdx.x;
+  Pad* const mine = a.pad[rank];
+  const uint64_t e = begin_epoch(mine);
+  __shared__ uint32_t s_k;
+  if (threadIdx.x == 0) s_k = ++mine->nvls_seq[b];
+  if (entry_barrier(a, rank, b, e)) {
+    constexpr int K = E::kPerVec;
+    const uint64_t nvec = a.count / K;
+    const uint64_t lo = nvec * rank / n, hi = nvec * (rank + 1) / n;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += stride) {
+      if constexpr (K == 8)
+        nvls_vec_bf16(a.mcbuf + i * 16, a.scale);
+      else
+        nvls_vec_f32(a.mcbuf + i * 16, a.scale);
+    }
+    // ragged tail (< K elements): the last rank folds it over unicast peers
+    const uint64_t t0 = nvec * K;
+    if (rank == n - 1 && b == 0 && threadIdx.x < a.count - t0) {
+      const uint64_t el = t0 + threadIdx.x;
+      float acc = E::load1(a.buf[0], el);
+      for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, E::load1(a.buf[r], el));
+      acc = __fmul_rn(acc, a.scale);
+      for (int r = 0; r < n; ++r) E::store1(a.buf[r], el, acc);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint32_t target = (uint32_t)n * s_k;
+      asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(a.mc_exit + b) : "memory");
+      uint64_t t_start = 0;
+      for (uint32_t it = 1;; ++it) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.uc_exit + b) : "memory");
+        if ((int32_t)(v - target) >= 0) break;
+        if ((it & 1023u) == 0) {
+          if (!t_start) t_start = globaltimer();
+          if (*a.err != 0) break;
+          if (globaltimer() - t_start > a.timeout_ns) {
+            raise_error(a, kErrTimeout);
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  end_epoch(mine, e);
 }
 
 // ---------------------------------------------------------------------------

@@ -70,8 +70,11 @@ struct Region {
   char* base[kMaxRanks] = {};
   bool opened[kMaxRanks] = {};  // base[r] came from cudaIpcOpenMemHandle
   bool owned = false;           // we cudaMalloc'ed base[local ranks]
+  bool nvls = false;            // the NVLS multicast arena (torn down by nvls_teardown)
   size_t bytes = 0;
 };
+
+struct Nvls;  // hfr_nvls.cuh
 
 struct IpcRecord {
   cudaIpcMemHandle_t handle;
@@ -115,6 +118,7 @@ struct hfr_comm_s {
   uint64_t ce_epoch = 0;
   uint64_t* trace = nullptr;  // hfr_set_trace (diagnostic)
   uint32_t trace_cap = 0;
+  Nvls* nvls = nullptr;       // NVLS multicast arena (hfr_config.nvls_bytes)
 };
 
 // ---------------------------------------------------------------------------
@@ -211,7 +215,7 @@ int effective_algo(const hfr_comm_s* c, size_t bytes) {
 }
 
 hfr_status_t validate_cfg(const hfr_config_t& c) {
-  if (c.algo < HFR_ALGO_AUTO || c.algo > HFR_ALGO_CE) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.algo < HFR_ALGO_AUTO || c.algo > HFR_ALGO_NVLS) return HFR_ERR_INVALID_ARGUMENT;
   if (c.oneshot_max_bytes > (64u << 20)) return HFR_ERR_INVALID_ARGUMENT;
   if (c.chunk_elems % 256 != 0 || c.chunk_elems > (1u << 30)) return HFR_ERR_INVALID_ARGUMENT;
   if (c.max_ctas < 0 || c.max_ctas > kMaxCtas) return HFR_ERR_INVALID_ARGUMENT;
@@ -300,6 +304,10 @@ hfr_status_t share_region(hfr_comm_s* c, char* ptr, size_t bytes, Region* out) {
 }
 
 void close_region(hfr_comm_s* c, Region& r) {
+  if (r.nvls) {  // mappings belong to the NVLS arena
+    r = Region();
+    return;
+  }
   for (int q = 0; q < c->n; ++q) {
     if (r.opened[q] && r.base[q]) {
       // the mapping was opened at the allocation base; recover it
@@ -366,6 +374,12 @@ hfr_status_t alloc_region(hfr_comm_s* c, size_t bytes, Region* out) {
   return HFR_SUCCESS;
 }
 
+}  // namespace
+
+#include "hfr_nvls.cuh"
+
+namespace {
+
 hfr_status_t common_init(hfr_comm_s* c) {
   HFR_CU(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->dev));
   HFR_CU(cudaHostAlloc((void**)&c->err_host, sizeof(uint32_t) * 4, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -389,6 +403,21 @@ hfr_status_t common_init(hfr_comm_s* c) {
   }
   HFR_TRY(alloc_region(c, sizeof(Pad), &c->pad));
   HFR_TRY(alloc_region(c, c->cfg.scratch_bytes, &c->scratch));
+  if (c->cfg.nvls_bytes > 0 && !c->virt && c->n > 1) {
+    c->nvls = new Nvls;
+    hfr_status_t st = nvls_setup(c, *c->nvls, c->cfg.nvls_bytes);
+    if (st == HFR_ERR_UNSUPPORTED) {
+      nvls_teardown(*c->nvls, c->n, c->rank);  // no NVLS on this box: NVLS calls report UNSUPPORTED
+    } else if (st != HFR_SUCCESS) {
+      return st;
+    } else {
+      Region r;
+      for (int q = 0; q < c->n; ++q) r.base[q] = (char*)c->nvls->uc[q];
+      r.bytes = c->nvls->size;
+      r.nvls = true;
+      c->regions.push_back(r);
+    }
+  }
   return HFR_SUCCESS;
 }
 
@@ -686,6 +715,23 @@ hfr_status_t run_ce(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_
   return ce_handshake(c, s, offsetof(Pad, ce_exit), e);
 }
 
+hfr_status_t run_nvls(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig, uint64_t offset,
+                      cudaStream_t s) {
+  const void* fn = dt == HFR_BFLOAT16 ? (const void*)hfr_nvls_kernel<BF16> : (const void*)hfr_nvls_kernel<F32>;
+  const int threads = c->cfg.threads;
+  const uint64_t per = dt == HFR_BFLOAT16 ? 8 : 4;
+  const uint64_t vec_per_rank = count / per / c->n + 1;
+  int g = 0;
+  HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>((vec_per_rank + threads - 1) / threads, kMaxCtas), &g));
+  Args a;
+  base_args(c, a, count, fnv(sig, (uint64_t)g * 1315423911ull + threads));
+  for (int q = 0; q < c->n; ++q) a.buf[q] = bufs[q];
+  a.mcbuf = (char*)c->nvls->mcva + offset;
+  a.mc_exit = (uint32_t*)c->nvls->mcva;
+  a.uc_exit = (uint32_t*)c->nvls->uc[c->rank];
+  return launch(c, fn, g, threads, a, s);
+}
+
 hfr_status_t run_copy(hfr_comm_s* c, char* dst, const char* src, uint64_t bytes, cudaStream_t s) {
   if (bytes == 0) return HFR_SUCCESS;
   const int threads = 512;
@@ -734,6 +780,7 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
   if (c->sticky != HFR_SUCCESS) return c->sticky;
   const int algo = effective_algo(c, count * dtype_size(dt));
   if (algo == HFR_ALGO_PAIR_DBT && c->n % 2 != 0) return HFR_ERR_UNSUPPORTED;
+  if (algo == HFR_ALGO_NVLS && (c->virt || !c->nvls || !c->nvls->on)) return HFR_ERR_UNSUPPORTED;
   for (int q = 0; q < c->local; ++q)
     if (count > 0 && !local_bufs[q]) return HFR_ERR_INVALID_ARGUMENT;
   DeviceGuard guard(c->dev);
@@ -797,7 +844,10 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     sig = fnv(sig, (uint64_t)zero_copy);
     sig = fnv(sig, algo == HFR_ALGO_FLAT ? 0 : c->cfg.chunk_elems);
     sig = fnv(sig, offset);
-    if (algo == HFR_ALGO_CE && zero_copy) {
+    if (algo == HFR_ALGO_NVLS) {
+      if (!zero_copy || !reg || !reg->nvls || !c->nvls || !c->nvls->on) return HFR_ERR_UNSUPPORTED;
+      HFR_TRY(run_nvls(c, bufs, count, dt, sig, offset, s));
+    } else if (algo == HFR_ALGO_CE && zero_copy) {
       HFR_TRY(run_ce(c, bufs, count, dt, s));
     } else if (algo == HFR_ALGO_FLAT || algo == HFR_ALGO_CE) {
       HFR_TRY(run_flat(c, bufs, count, dt, sig, s));
@@ -895,6 +945,7 @@ hfr_status_t hfr_comm_set_config(hfr_comm_t c, const hfr_config_t* cfg) {
   n.scratch_bytes = c->cfg.scratch_bytes;
   n.timeout_ms = c->cfg.timeout_ms;
   n.oneshot_max_bytes = c->cfg.oneshot_max_bytes;
+  n.nvls_bytes = c->cfg.nvls_bytes;
   resolve_defaults(n);
   c->cfg = n;
   return HFR_SUCCESS;
@@ -909,6 +960,12 @@ hfr_status_t hfr_mem_alloc(hfr_comm_t c, size_t bytes, void** ptrs) {
   if (!c) return HFR_ERR_NOT_INITIALIZED;
   if (!ptrs || bytes == 0) return HFR_ERR_INVALID_ARGUMENT;
   DeviceGuard guard(c->dev);
+  if (c->nvls && c->nvls->on && c->nvls->used + bytes <= c->nvls->size) {
+    // symmetric bump allocation inside the NVLS arena (same offsets on every rank)
+    ptrs[0] = (void*)(c->nvls->uc[c->rank] + c->nvls->used);
+    c->nvls->used += round_up(bytes, 4096);
+    return HFR_SUCCESS;
+  }
   Region r;
   HFR_TRY(alloc_region(c, bytes, &r));
   c->regions.push_back(r);
@@ -919,6 +976,9 @@ hfr_status_t hfr_mem_alloc(hfr_comm_t c, size_t bytes, void** ptrs) {
 hfr_status_t hfr_mem_free(hfr_comm_t c, void* ptr) {
   if (!c) return HFR_ERR_NOT_INITIALIZED;
   DeviceGuard guard(c->dev);
+  if (c->nvls && c->nvls->on && (CUdeviceptr)ptr >= c->nvls->uc[c->rank] &&
+      (CUdeviceptr)ptr < c->nvls->uc[c->rank] + c->nvls->size)
+    return HFR_SUCCESS;  // arena memory lives until hfr_finalize
   for (size_t i = 0; i < c->regions.size(); ++i) {
     Region& r = c->regions[i];
     if (r.owned && r.base[c->virt ? 0 : c->rank] == ptr) {
@@ -1018,6 +1078,10 @@ hfr_status_t hfr_finalize(hfr_comm_t c) {
     c->regions.clear();
     close_region(c, c->scratch);
     close_region(c, c->pad);
+    if (c->nvls) {
+      nvls_teardown(*c->nvls, c->n, c->rank);
+      delete c->nvls;
+    }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     for (cudaStream_t h : c->helpers) cudaStreamDestroy(h);
     for (cudaEvent_t e : c->ce_events) cudaEventDestroy(e);

@@ -48,3 +48,28 @@ def assert_bit_exact(got: np.ndarray, want: np.ndarray, what: str = ""):
         idx = np.flatnonzero(m)[bad[:5]]
         raise AssertionError(f"{what}: {bad.size} mismatching elements, first at {idx.tolist()}: "
                              f"got {g[idx].tolist()} want {w[idx].tolist()}")
+
+
+def assert_within_r18(got: np.ndarray, xs, want: np.ndarray, scale: float, what: str = ""):
+    """DESIGN.md reading R18 (order-relaxed paths): with A = sum_r |x_r| per
+    element, fp32 |got - want| <= 1e-6 * scale * A; bf16 |got - want| <=
+    max(1 ulp(want), 8.3e-7 * scale * A + 1/2 ulp(want)).  NaN/Inf positions
+    must match."""
+    g = as_f32(got).astype(np.float64)
+    w = as_f32(want).astype(np.float64)
+    A = np.zeros_like(w)
+    for x in xs:
+        A += np.abs(as_f32(x).astype(np.float64))
+    A *= abs(scale)
+    fin = np.isfinite(w)
+    assert np.array_equal(np.isnan(g), np.isnan(w)), f"{what}: NaN positions"
+    assert np.array_equal(g[~fin], w[~fin]) or not (~fin).any(), f"{what}: Inf mismatch"
+    d = np.abs(g[fin] - w[fin])
+    if got.dtype == np.uint16:
+        ex = np.floor(np.log2(np.maximum(np.abs(w[fin]), 2.0 ** -126)))
+        ulp = 2.0 ** (ex - 7)
+        lim = np.maximum(ulp, 8.3e-7 * A[fin] + 0.5 * ulp)
+    else:
+        lim = 1e-6 * A[fin]
+    bad = np.flatnonzero(d > lim)
+    assert bad.size == 0, f"{what}: {bad.size} elements beyond R18, worst {float((d - lim).max())}"

@@ -32,7 +32,7 @@ def gpu_cases(rank, world, port, outdir):
     import hfr_inputs as gen
     import paper_2408_14158_b200 as hfr
     from oracle import hfr_oracle as O
-    from tests.gpu_util import assert_bit_exact, to_numpy, to_torch, torch_dtype
+    from tests.gpu_util import assert_bit_exact, assert_within_r18, to_numpy, to_torch, torch_dtype
 
     torch.cuda.set_device(rank)
     _setup(rank, world, port, "gloo")
@@ -102,6 +102,51 @@ def gpu_cases(rank, world, port, outdir):
                 res["ok"].append("protocol")
             else:
                 res["fail"].append(f"protocol: got {e}")
+        comm.finalize()
+        # NVLS order-relaxed path (reading R18 bound), if the box has multicast
+        comm = hfr.Comm.init(device=rank, config=hfr.Config(timeout_ms=8000, nvls_bytes=64 << 20, algo="nvls",
+                                                            scale=0.5))
+        for dtype in (gen.FP32, gen.BF16):
+            for N in (4096 + 13, 1_000_003):
+                for dist_name in ("normal", "int"):
+                    xs = gen.rank_inputs(world, N, dtype, dist_name, seed_base=5000 + N)
+                    t = comm.empty(N, torch_dtype(dtype))
+                    t.copy_(to_torch(xs[rank], t.device))
+                    name = f"nvls/{dtype}/{N}/{dist_name}"
+                    try:
+                        comm.allreduce(t)
+                    except hfr.HfrError as e:
+                        if e.status == hfr.ERR_UNSUPPORTED:
+                            res["ok"].append("nvls-unsupported")
+                            break
+                        raise
+                    torch.cuda.synchronize()
+                    got = to_numpy(t)
+                    want = O.fold_ascending(xs, 0.5)
+                    try:
+                        if dist_name == "int":
+                            assert_bit_exact(got, want, name)  # exact sums: every order agrees
+                        else:
+                            assert_within_r18(got, xs, want, 0.5, name)
+                        h = hashlib.sha256(got.tobytes()).hexdigest()
+                        hs = [None] * world
+                        dist.all_gather_object(hs, h)
+                        assert len(set(hs)) == 1, f"{name}: ranks differ"
+                        res["ok"].append(name)
+                    except AssertionError as e:
+                        res["fail"].append(str(e)[:500])
+        # every other schedule also runs zero-copy on NVLS arena memory
+        comm.set_config(hfr.Config(algo="flat", scale=0.5))
+        xs = gen.rank_inputs(world, 100_000, gen.FP32, "normal", seed_base=77)
+        t = comm.empty(100_000, torch.float32)
+        t.copy_(to_torch(xs[rank], t.device))
+        comm.allreduce(t)
+        torch.cuda.synchronize()
+        try:
+            assert_bit_exact(to_numpy(t), O.fold_ascending(xs, 0.5), "flat-on-nvls-arena")
+            res["ok"].append("flat-on-nvls-arena")
+        except AssertionError as e:
+            res["fail"].append(str(e)[:500])
         comm.finalize()
         # timeout: rank 0 calls alone
         comm = hfr.Comm.init(device=rank, config=hfr.Config(timeout_ms=1500))
