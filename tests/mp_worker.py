@@ -124,8 +124,8 @@ def gpu_cases(rank, world, port, outdir):
                     got = to_numpy(t)
                     want = O.fold_ascending(xs, 0.5)
                     try:
-                        if dist_name == "int":
-                            assert_bit_exact(got, want, name)  # exact sums: every order agrees
+                        if dist_name == "int" and dtype == gen.FP32:
+                            assert_bit_exact(got, want, name)  # exact fp32 sums: every order agrees
                         else:
                             assert_within_r18(got, xs, want, 0.5, name)
                         h = hashlib.sha256(got.tobytes()).hexdigest()

@@ -33,6 +33,7 @@ def main():
     p.add_argument("--iters", type=int, default=0)
     p.add_argument("--nccl", action="store_true")
     p.add_argument("--graph", action="store_true", help="time `iters` calls captured in one CUDA graph")
+    p.add_argument("--nvls", type=int, default=0, help="NVLS arena bytes per rank (enables algo nvls)")
     p.add_argument("--out", default="")
     a = p.parse_args()
 
@@ -55,7 +56,8 @@ def main():
     tdt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
     esz = 2 if a.dtype == "bf16" else 4
     sizes = [int(s) for s in a.sizes.split(",")]
-    comm = hfr.Comm.init(device=local) if multi else hfr.Comm.virtual_ranks(n, local)
+    comm = (hfr.Comm.init(device=local, config=hfr.Config(nvls_bytes=a.nvls)) if multi
+            else hfr.Comm.virtual_ranks(n, local))
     big = max(sizes) // esz
     bufs = comm.empty(big, tdt)
     bufs = bufs if isinstance(bufs, list) else [bufs]
