@@ -225,7 +225,16 @@ def main():
     scale = 1.0 / n
     cfg = hfr.Config(algo=args.algo, scale=scale, max_ctas=args.max_ctas, threads=args.threads,
                      timeout_ms=30000)
-    comm = hfr.Comm.init(device=local, config=cfg) if multi else hfr.Comm.virtual_ranks(n, local, cfg)
+    nvls_note = None
+    if multi:
+        # NVLS arena (order-relaxed variant) holds the bench buffer; FLAT runs on it zero-copy too
+        try:
+            comm = hfr.Comm.init(device=local, config=hfr.Config(**{**cfg.__dict__, "nvls_bytes": S + (64 << 20)}))
+        except hfr.HfrError as e:
+            nvls_note = f"no NVLS arena: {e}"
+            comm = hfr.Comm.init(device=local, config=cfg)
+    else:
+        comm = hfr.Comm.virtual_ranks(n, local, cfg)
     stream = torch.cuda.current_stream()
 
     # inputs: this process's ranks
@@ -363,15 +372,23 @@ def main():
         del t
     variants = {}
     if multi and not args.no_variants:  # tree schedules over NVLink (virtual-rank trees are not meaningful)
-        for algo in ("dbt", "pair_dbt"):
+        for algo in ("dbt", "pair_dbt", "nvls"):
             if algo == args.algo or (algo == "pair_dbt" and n % 2):
                 continue
             comm.set_config(hfr.Config(algo=algo, scale=scale, max_ctas=args.max_ctas, threads=args.threads,
                                        timeout_ms=30000))
-            for _ in range(2):
-                step()
+            try:
+                for _ in range(2):
+                    step()
+            except hfr.HfrError as e:
+                variants[algo] = {"unavailable": nvls_note or str(e)}
+                continue
             tv, _ = timed(step, max(3, args.steps // 2))
             variants[algo] = {"busbw": busbw(S, tv, n), "ms_per_step": tv * 1e3}
+            if algo == "nvls":
+                variants[algo]["numerics"] = "order-relaxed (NVSwitch reduction), held to DESIGN.md R18, not bit-exact"
+            else:
+                variants[algo]["numerics"] = "bit-exact vs the tree-order / pair-first oracle"
         comm.set_config(cfg)
 
     cpu = None

@@ -478,36 +478,53 @@ __global__ void __launch_bounds__(512) hfr_oneshot_kernel(const Args a) {
 // handshake (argument check); exit: one multimem.red.release per CTA bumps
 // counter b on every GPU, each CTA waits until all n ranks' CTA b arrived.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void nvls_vec_f32(char* mc, float scale) {
-  float x, y, z, w;
-  asm volatile("multimem.ld_reduce.weak.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=f"(x), "=f"(y), "=f"(z), "=f"(w)
-               : "l"(mc)
-               : "memory");
-  x = __fmul_rn(x, scale);
-  y = __fmul_rn(y, scale);
-  z = __fmul_rn(z, scale);
-  w = __fmul_rn(w, scale);
-  asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "f"(x), "f"(y), "f"(z), "f"(w)
-               : "memory");
+// U multimem.ld_reduce in flight per thread before the first multimem.st
+template <int U>
+__device__ __forceinline__ void nvls_vecs_f32(char* mc, uint64_t stride_bytes, int cnt, float scale) {
+  float v[U][4];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (u < cnt)
+      asm volatile("multimem.ld_reduce.weak.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(v[u][0]), "=f"(v[u][1]), "=f"(v[u][2]), "=f"(v[u][3])
+                   : "l"(mc + u * stride_bytes)
+                   : "memory");
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (u < cnt) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[u][k] = __fmul_rn(v[u][k], scale);
+      asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc + u * stride_bytes), "f"(v[u][0]),
+                   "f"(v[u][1]), "f"(v[u][2]), "f"(v[u][3])
+                   : "memory");
+    }
 }
 
-__device__ __forceinline__ void nvls_vec_bf16(char* mc, float scale) {
-  uint4 v;
-  asm volatile("multimem.ld_reduce.weak.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(mc)
-               : "memory");
-  if (scale != 1.0f) {
-    float f[8];
-    BF16::widen(v, f);
+template <int U>
+__device__ __forceinline__ void nvls_vecs_bf16(char* mc, uint64_t stride_bytes, int cnt, float scale) {
+  uint4 v[U];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(f[k], scale);
-    v = BF16::narrow(f);
-  }
-  asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "f"(__uint_as_float(v.x)),
-               "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
-               : "memory");
+  for (int u = 0; u < U; ++u)
+    if (u < cnt)
+      asm volatile("multimem.ld_reduce.weak.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                   : "l"(mc + u * stride_bytes)
+                   : "memory");
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (u < cnt) {
+      if (scale != 1.0f) {
+        float f[8];
+        BF16::widen(v[u], f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(f[k], scale);
+        v[u] = BF16::narrow(f);
+      }
+      asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc + u * stride_bytes),
+                   "f"(__uint_as_float(v[u].x)), "f"(__uint_as_float(v[u].y)), "f"(__uint_as_float(v[u].z)),
+                   "f"(__uint_as_float(v[u].w))
+                   : "memory");
+    }
 }
 
 template <class E>
@@ -524,11 +541,13 @@ __global__ void __launch_bounds__(512) hfr_nvls_kernel(const Args a) {
     const uint64_t nvec = a.count / K;
     const uint64_t lo = nvec * rank / n, hi = nvec * (rank + 1) / n;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += stride) {
+    constexpr int U = 4;
+    for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += U * stride) {
+      const int cnt = (int)((hi - i + stride - 1) / stride);
       if constexpr (K == 8)
-        nvls_vec_bf16(a.mcbuf + i * 16, a.scale);
+        nvls_vecs_bf16<U>(a.mcbuf + i * 16, stride * 16, cnt, a.scale);
       else
-        nvls_vec_f32(a.mcbuf + i * 16, a.scale);
+        nvls_vecs_f32<U>(a.mcbuf + i * 16, stride * 16, cnt, a.scale);
     }
     // ragged tail (< K elements): the last rank folds it over unicast peers
     const uint64_t t0 = nvec * K;
