@@ -78,8 +78,9 @@ def main():
         params = [p for p in params if not p[0].startswith("l") or p[0][:p[0].index(".") + 1] in keep
                   or p[0].startswith("lm_head")]
     numels = [o * i for _, o, i in params]
+    nvls = (TOTAL * 2 + (256 << 20)) if a.algo == "nvls" else 0
     comm = hfr.Comm.init(device=local, config=hfr.Config(algo=a.algo, max_ctas=a.max_ctas, scale=1.0 / world,
-                                                        stream_gate=a.gate))
+                                                        stream_gate=a.gate, nvls_bytes=nvls))
     ddp = HaiScaleDDP(comm, numels, torch.bfloat16, bucket_bytes=a.bucket_mib << 20)
     T = a.tokens
     g = torch.Generator(device=dev).manual_seed(3000 + rank)
