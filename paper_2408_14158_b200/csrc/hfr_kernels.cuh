@@ -467,6 +467,98 @@ __global__ void __launch_bounds__(512) hfr_oneshot_kernel(const Args a) {
 }
 
 // ---------------------------------------------------------------------------
+// ONESHOT, LL form (messages <= 64 KiB): the flag travels inside the data.
+//
+// Every element becomes one 8-byte word {element bits, flag}, flag =
+// (sig8 << 24) | (epoch & 0xFFFFFF); two words go out per 16-byte store, so a
+// word is never seen half-written.  A receiver spins on the words of its
+// slice until every source's flag shows this launch, then folds in rank order
+// (the FLAT bits again).  No fence, no separate handshake: latency is one
+// NVLink write.  Slot reuse (parity = epoch & 1) is safe for the same reason
+// as the fenced ONESHOT: a rank only enters launch e+2 after it received
+// every peer's launch-e+1 data, which peers send after finishing launch e.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ld128_volatile(const void* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p)
+               : "memory");
+  return v;
+}
+
+template <class E>
+__device__ __forceinline__ uint32_t elem_bits(const char* p, uint64_t e) {
+  if constexpr (E::kPerVec == 8) return reinterpret_cast<const uint16_t*>(p)[e];
+  return reinterpret_cast<const uint32_t*>(p)[e];
+}
+template <class E>
+__device__ __forceinline__ float bits_value(uint32_t b) {
+  if constexpr (E::kPerVec == 8) return __uint_as_float(b << 16);
+  return __uint_as_float(b);
+}
+
+template <class E>
+__global__ void __launch_bounds__(512) hfr_oneshot_ll_kernel(const Args a) {
+  const int rank = a.rank0 + blockIdx.y;
+  const int n = a.n;
+  const int b = blockIdx.x;
+  const uint64_t ep = begin_epoch(a.pad[rank]);
+  const uint32_t sig8 = (uint32_t)(a.sig ^ (a.sig >> 32)) & 0xFFu;
+  const uint32_t flag = (sig8 << 24) | (uint32_t)(ep & 0xFFFFFFu);
+  const uint64_t par = ep & 1;
+  const uint64_t npair = (a.count + 1) / 2;
+  const uint64_t p0 = npair * b / gridDim.x, p1 = npair * (b + 1) / gridDim.x;
+  const char* src = a.buf[rank];
+  // 1. push {x, flag} words for this CTA's pairs into every rank's slot [par][rank]
+  for (uint64_t i = p0 + threadIdx.x; i < p1; i += blockDim.x) {
+    const uint64_t e = 2 * i;
+    const uint32_t x0 = elem_bits<E>(src, e);
+    const uint32_t x1 = e + 1 < a.count ? elem_bits<E>(src, e + 1) : 0u;
+    const uint4 w = make_uint4(x0, flag, x1, flag);
+    for (int q = 0; q < n; ++q) st128(a.inbox[q] + (par * n + rank) * a.slot_bytes + i * 16, w);
+  }
+  // 2. receive and fold
+  const char* in = a.inbox[rank] + par * n * a.slot_bytes;
+  char* dst = a.buf[rank];
+  bool ok = true;
+  for (uint64_t i = p0 + threadIdx.x; i < p1 && ok; i += blockDim.x) {
+    float acc0 = 0.f, acc1 = 0.f;
+    for (int r = 0; r < n && ok; ++r) {
+      const char* w_at = in + r * a.slot_bytes + i * 16;
+      uint4 w = ld128_volatile(w_at);
+      uint64_t t0 = 0;
+      for (uint32_t it = 1; ((w.y & 0xFFFFFFu) != (flag & 0xFFFFFFu)) || ((w.w & 0xFFFFFFu) != (flag & 0xFFFFFFu));
+           ++it) {
+        if ((it & 1023u) == 0) {
+          if (!t0) t0 = globaltimer();
+          if (*a.err != 0 || globaltimer() - t0 > a.timeout_ns) {
+            if (*a.err == 0) raise_error(a, kErrTimeout);
+            ok = false;
+            break;
+          }
+        }
+        w = ld128_volatile(w_at);
+      }
+      if (!ok) break;
+      if ((w.y >> 24) != sig8 || (w.w >> 24) != sig8) {
+        raise_error(a, kErrProtocol);
+        ok = false;
+        break;
+      }
+      const float v0 = bits_value<E>(w.x), v1 = bits_value<E>(w.z);
+      acc0 = r == 0 ? v0 : __fadd_rn(acc0, v0);
+      acc1 = r == 0 ? v1 : __fadd_rn(acc1, v1);
+    }
+    if (!ok) break;
+    const uint64_t e = 2 * i;
+    E::store1(dst, e, __fmul_rn(acc0, a.scale));
+    if (e + 1 < a.count) E::store1(dst, e + 1, __fmul_rn(acc1, a.scale));
+  }
+  end_epoch(a.pad[rank], ep);
+}
+
+// ---------------------------------------------------------------------------
 // NVLS (order-relaxed; hfr_nvls.cuh): the NVSwitch reduces and multicasts.
 //
 // Rank g owns shard g.  Per 16 B: one multimem.ld_reduce on the multicast

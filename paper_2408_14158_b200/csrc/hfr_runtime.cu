@@ -581,8 +581,28 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   return HFR_SUCCESS;
 }
 
+constexpr uint64_t kLLMaxBytes = 64u << 10;  // ONESHOT uses the LL (flag-in-data) form up to here
+
+hfr_status_t run_oneshot_ll(hfr_comm_s* c, char* const* local_bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
+                            cudaStream_t s) {
+  const void* fn = dt == HFR_BFLOAT16 ? (const void*)hfr_oneshot_ll_kernel<BF16> : (const void*)hfr_oneshot_ll_kernel<F32>;
+  const uint64_t npair = (count + 1) / 2;
+  const int threads = (int)std::max<uint64_t>(32, std::min<uint64_t>(256, round_up(npair, 32)));
+  int g = 0;
+  HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>((npair + 1023) / 1024, kMaxCtas), &g));
+  Args a;
+  base_args(c, a, count, fnv(sig, 0x11ull + (uint64_t)g * 1315423911ull + threads));
+  a.slot_bytes = c->cfg.oneshot_max_bytes;
+  for (int q = 0; q < c->n; ++q) a.inbox[q] = c->scratch.base[q];
+  for (int q = 0; q < c->local; ++q) a.buf[c->virt ? q : c->rank] = local_bufs[q];
+  return launch(c, fn, g, threads, a, s);
+}
+
 hfr_status_t run_oneshot(hfr_comm_s* c, char* const* local_bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                          cudaStream_t s) {
+  // LL form: 8 inbox bytes per element, one NVLink write of latency
+  if (count * dtype_size(dt) <= kLLMaxBytes && count * 8 <= c->cfg.oneshot_max_bytes)
+    return run_oneshot_ll(c, local_bufs, count, dt, sig, s);
   const void* fn = dt == HFR_BFLOAT16 ? (const void*)hfr_oneshot_kernel<BF16, 0> : (const void*)hfr_oneshot_kernel<F32, 0>;
   const uint64_t per = dt == HFR_BFLOAT16 ? 8 : 4;
   const uint64_t nvec = count / per;

@@ -170,10 +170,12 @@ def test_bf16_exhaustive_n2_sample(hfr):
 
 
 @pytest.mark.parametrize("algo", ALGOS)
-def test_cuda_graph_replay(hfr, algo):
+@pytest.mark.parametrize("N", [2_003, 20_003])
+def test_cuda_graph_replay(hfr, algo, N):
     """Captured allreduces replay correctly (device-side launch epochs): k
-    replays of one captured in-place allreduce == the oracle applied k times."""
-    n, N = 4, 20_000 + 3
+    replays of one captured in-place allreduce == the oracle applied k times.
+    N=2003 runs ONESHOT's LL (flag-in-data) form, N=20003 the fenced form."""
+    n = 4
     comm = comm_for(hfr, n)
     comm.set_config(hfr.Config(algo=algo, chunk_elems=512, scale=0.25))
     xs = gen.rank_inputs(n, N, gen.FP32, "normal", seed_base=66)
