@@ -499,56 +499,68 @@ __device__ __forceinline__ float bits_value(uint32_t b) {
 }
 
 template <class E>
+__device__ __forceinline__ bool ll_ready(const uint4& w, uint32_t flag) {
+  return ((w.y ^ flag) & 0xFFFFFFu) == 0 && ((w.w ^ flag) & 0xFFFFFFu) == 0;
+}
+
+// NR = compile-time rank count (2, 4, 8) so all n words of a pair are loaded
+// at once; 0 = runtime n (one source at a time).
+template <class E, int NR>
 __global__ void __launch_bounds__(512) hfr_oneshot_ll_kernel(const Args a) {
   const int rank = a.rank0 + blockIdx.y;
-  const int n = a.n;
-  const int b = blockIdx.x;
+  const int n = NR > 0 ? NR : a.n;
   const uint64_t ep = begin_epoch(a.pad[rank]);
   const uint32_t sig8 = (uint32_t)(a.sig ^ (a.sig >> 32)) & 0xFFu;
   const uint32_t flag = (sig8 << 24) | (uint32_t)(ep & 0xFFFFFFu);
   const uint64_t par = ep & 1;
   const uint64_t npair = (a.count + 1) / 2;
-  const uint64_t p0 = npair * b / gridDim.x, p1 = npair * (b + 1) / gridDim.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const char* src = a.buf[rank];
-  // 1. push {x, flag} words for this CTA's pairs into every rank's slot [par][rank]
-  for (uint64_t i = p0 + threadIdx.x; i < p1; i += blockDim.x) {
+  // 1. push {x, flag} words of my pairs into every rank's slot [par][rank]
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npair; i += stride) {
     const uint64_t e = 2 * i;
     const uint32_t x0 = elem_bits<E>(src, e);
     const uint32_t x1 = e + 1 < a.count ? elem_bits<E>(src, e + 1) : 0u;
     const uint4 w = make_uint4(x0, flag, x1, flag);
     for (int q = 0; q < n; ++q) st128(a.inbox[q] + (par * n + rank) * a.slot_bytes + i * 16, w);
   }
-  // 2. receive and fold
+  // 2. receive (all n words of a pair in flight at once) and fold in rank order
   const char* in = a.inbox[rank] + par * n * a.slot_bytes;
   char* dst = a.buf[rank];
   bool ok = true;
-  for (uint64_t i = p0 + threadIdx.x; i < p1 && ok; i += blockDim.x) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npair && ok; i += stride) {
+    constexpr int M = NR > 0 ? NR : 1;
+    uint4 w[M];
     float acc0 = 0.f, acc1 = 0.f;
-    for (int r = 0; r < n && ok; ++r) {
-      const char* w_at = in + r * a.slot_bytes + i * 16;
-      uint4 w = ld128_volatile(w_at);
+    for (int r0 = 0; r0 < n && ok; r0 += M) {
+#pragma unroll
+      for (int u = 0; u < M; ++u) w[u] = ld128_volatile(in + (r0 + u) * a.slot_bytes + i * 16);
       uint64_t t0 = 0;
-      for (uint32_t it = 1; ((w.y & 0xFFFFFFu) != (flag & 0xFFFFFFu)) || ((w.w & 0xFFFFFFu) != (flag & 0xFFFFFFu));
-           ++it) {
-        if ((it & 1023u) == 0) {
-          if (!t0) t0 = globaltimer();
-          if (*a.err != 0 || globaltimer() - t0 > a.timeout_ns) {
-            if (*a.err == 0) raise_error(a, kErrTimeout);
-            ok = false;
-            break;
+#pragma unroll
+      for (int u = 0; u < M; ++u) {
+        for (uint32_t it = 1; !ll_ready<E>(w[u], flag); ++it) {
+          if ((it & 1023u) == 0) {
+            if (!t0) t0 = globaltimer();
+            if (*a.err != 0 || globaltimer() - t0 > a.timeout_ns) {
+              if (*a.err == 0) raise_error(a, kErrTimeout);
+              ok = false;
+              break;
+            }
           }
+          w[u] = ld128_volatile(in + (r0 + u) * a.slot_bytes + i * 16);
         }
-        w = ld128_volatile(w_at);
+        if (ok && ((w[u].y >> 24) != sig8 || (w[u].w >> 24) != sig8)) {
+          raise_error(a, kErrProtocol);
+          ok = false;
+        }
       }
       if (!ok) break;
-      if ((w.y >> 24) != sig8 || (w.w >> 24) != sig8) {
-        raise_error(a, kErrProtocol);
-        ok = false;
-        break;
+#pragma unroll
+      for (int u = 0; u < M; ++u) {
+        const float v0 = bits_value<E>(w[u].x), v1 = bits_value<E>(w[u].z);
+        acc0 = r0 + u == 0 ? v0 : __fadd_rn(acc0, v0);
+        acc1 = r0 + u == 0 ? v1 : __fadd_rn(acc1, v1);
       }
-      const float v0 = bits_value<E>(w.x), v1 = bits_value<E>(w.z);
-      acc0 = r == 0 ? v0 : __fadd_rn(acc0, v0);
-      acc1 = r == 0 ? v1 : __fadd_rn(acc1, v1);
     }
     if (!ok) break;
     const uint64_t e = 2 * i;

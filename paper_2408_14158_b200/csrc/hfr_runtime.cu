@@ -585,11 +585,19 @@ constexpr uint64_t kLLMaxBytes = 64u << 10;  // ONESHOT uses the LL (flag-in-dat
 
 hfr_status_t run_oneshot_ll(hfr_comm_s* c, char* const* local_bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                             cudaStream_t s) {
-  const void* fn = dt == HFR_BFLOAT16 ? (const void*)hfr_oneshot_ll_kernel<BF16> : (const void*)hfr_oneshot_ll_kernel<F32>;
+  const bool bf = dt == HFR_BFLOAT16;
+  const void* fn;
+  switch (c->n) {
+    case 2: fn = bf ? (const void*)hfr_oneshot_ll_kernel<BF16, 2> : (const void*)hfr_oneshot_ll_kernel<F32, 2>; break;
+    case 4: fn = bf ? (const void*)hfr_oneshot_ll_kernel<BF16, 4> : (const void*)hfr_oneshot_ll_kernel<F32, 4>; break;
+    case 8: fn = bf ? (const void*)hfr_oneshot_ll_kernel<BF16, 8> : (const void*)hfr_oneshot_ll_kernel<F32, 8>; break;
+    default: fn = bf ? (const void*)hfr_oneshot_ll_kernel<BF16, 0> : (const void*)hfr_oneshot_ll_kernel<F32, 0>;
+  }
   const uint64_t npair = (count + 1) / 2;
+  // one pair per thread: every word's latency overlaps every other's
   const int threads = (int)std::max<uint64_t>(32, std::min<uint64_t>(256, round_up(npair, 32)));
   int g = 0;
-  HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>((npair + 1023) / 1024, kMaxCtas), &g));
+  HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>((npair + threads - 1) / threads, kMaxCtas), &g));
   Args a;
   base_args(c, a, count, fnv(sig, 0x11ull + (uint64_t)g * 1315423911ull + threads));
   a.slot_bytes = c->cfg.oneshot_max_bytes;
