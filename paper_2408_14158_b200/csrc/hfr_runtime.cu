@@ -202,15 +202,17 @@ uint64_t fnv(uint64_t h, uint64_t v) {
 
 size_t dtype_size(hfr_dtype_t t) { return t == HFR_BFLOAT16 ? 2 : 4; }
 
-// AUTO: ONESHOT up to oneshot_max_bytes, FLAT above; an explicit ONESHOT on a
-// larger message also runs FLAT (same result bits).
+// An explicit ONESHOT on a message above oneshot_max_bytes runs FLAT (same
+// result bits).
 int effective_algo(const hfr_comm_s* c, size_t bytes) {
   const int a = c->cfg.algo;
   // CE needs separate processes (stream waits across ranks) and shards of at
   // least 4096 elements; otherwise it runs FLAT (same bits)
   if (a == HFR_ALGO_CE) return (c->virt || c->n == 1 || bytes < (size_t)c->n * 16384) ? HFR_ALGO_FLAT : HFR_ALGO_CE;
-  if (a == HFR_ALGO_AUTO || a == HFR_ALGO_ONESHOT)
-    return bytes <= c->cfg.oneshot_max_bytes ? HFR_ALGO_ONESHOT : HFR_ALGO_FLAT;
+  // AUTO: ONESHOT only in its LL form (<= 64 KiB, ~5 us on 4 B200s); above
+  // that FLAT is faster than the fenced ONESHOT (r01 graph sweep)
+  if (a == HFR_ALGO_AUTO) return bytes <= std::min<size_t>(64u << 10, c->cfg.oneshot_max_bytes / 8 * 2) ? HFR_ALGO_ONESHOT : HFR_ALGO_FLAT;
+  if (a == HFR_ALGO_ONESHOT) return bytes <= c->cfg.oneshot_max_bytes ? HFR_ALGO_ONESHOT : HFR_ALGO_FLAT;
   return a;
 }
 
