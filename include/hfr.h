@@ -216,10 +216,11 @@ hfr_status_t hfr_finalize(hfr_comm_t comm);
 hfr_status_t hfr_tree_query(int n, int which, int* parent, int* child0, int* child1);
 
 /* Diagnostic: record per-CTA chunk timelines of the tree schedules into
- * `dev_buf` (device memory, >= 32 * 1024 * local_ranks bytes; capacity per CTA
- * = bytes / (32 * 1024 * local_ranks) events of 4 u64 {tag, t_wait, t_work,
- * t_done} in globaltimer ns, CTA slot = local_rank * 1024 + cta).  NULL turns
- * tracing off.  Not for production use (adds timer reads). */
+ * `dev_buf` (device memory, >= 64 * 1024 * local_ranks bytes; capacity per CTA
+ * = bytes / (64 * 1024 * local_ranks) events of 8 u64 {tag, t_wait, t_work,
+ * t_stores_issued, t_done, 0, 0, 0} in globaltimer ns, CTA slot =
+ * local_rank * 1024 + cta).  NULL turns tracing off.  Not for production use
+ * (adds timer reads). */
 hfr_status_t hfr_set_trace(hfr_comm_t comm, void* dev_buf, size_t bytes);
 
 /* Kernel launches this comm has issued (for bench.py's gpu_launches). */

@@ -82,22 +82,25 @@ struct Args {
 };
 
 // Diagnostic per-CTA event log (hfr_set_trace): thread 0 records
-// {tag, t_wait_start, t_work_start, t_done} in globaltimer ns.
+// {tag, t_wait_start, t_work_start, t_stores_issued, t_done, 0, 0, 0} in
+// globaltimer ns (t_stores_issued: after the CTA barrier that follows the
+// chunk's stores, before the system fence that drains them).
 struct Tracer {
   uint64_t* p = nullptr;
   uint32_t cap = 0, n = 0;
   __device__ explicit Tracer(const Args& a) {
     if (a.trace && threadIdx.x == 0) {
       cap = a.trace_cap;
-      p = a.trace + ((uint64_t)blockIdx.y * kMaxCtas + blockIdx.x) * cap * 4;
+      p = a.trace + ((uint64_t)blockIdx.y * kMaxCtas + blockIdx.x) * cap * 8;
     }
   }
-  __device__ __forceinline__ void rec(uint64_t tag, uint64_t t0, uint64_t t1, uint64_t t2) {
+  __device__ __forceinline__ void rec(uint64_t tag, uint64_t t0, uint64_t t1, uint64_t t2, uint64_t t3) {
     if (p && n < cap) {
-      p[4 * n] = tag;
-      p[4 * n + 1] = t0;
-      p[4 * n + 2] = t1;
-      p[4 * n + 3] = t2;
+      p[8 * n] = tag;
+      p[8 * n + 1] = t0;
+      p[8 * n + 2] = t1;
+      p[8 * n + 3] = t2;
+      p[8 * n + 4] = t3;
       ++n;
     }
   }
@@ -772,7 +775,38 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     // the first add, so a CTA keeps TU x (2..4) x 32 B per thread in flight.
     constexpr int TU = 1;
     const int nchild = nd.nchild, self_pos = nd.self_pos;
-    for (uint64_t v0 = threadIdx.x; v0 < nv; v0 += (uint64_t)blockDim.x * TU) {
+#if HFR_VARIANT_LEAFCOPY
+    // experiment: a leaf's partial is its own x widened to fp32 — stream it
+    // as a copy with 4 x 16 B in flight per thread
+    const bool leafcopy = !PAIR && nchild == 0 && !root;
+#else
+    const bool leafcopy = false;
+#endif
+    if (leafcopy) {
+      const uint64_t nq = nv * 2;  // 16 B fp32 quads
+      for (uint64_t q0 = threadIdx.x; q0 < nq; q0 += (uint64_t)blockDim.x * 4) {
+        float f[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint64_t q = q0 + (uint64_t)u * blockDim.x;
+          if (q < nq) {
+            if constexpr (E::kPerVec == 8) {
+              const uint2 h = *reinterpret_cast<const uint2*>(mybuf + (base + e0 + q * 4) * 2);
+              f[u][0] = __uint_as_float(h.x << 16); f[u][1] = __uint_as_float(h.x & 0xFFFF0000u);
+              f[u][2] = __uint_as_float(h.y << 16); f[u][3] = __uint_as_float(h.y & 0xFFFF0000u);
+            } else {
+              F32::widen(ld128(mybuf + (base + e0 + q * 4) * 4), f[u]);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint64_t q = q0 + (uint64_t)u * blockDim.x;
+          if (q < nq) st128(dst_part + e0 + q * 4, F32::narrow(f[u]));
+        }
+      }
+    }
+    for (uint64_t v0 = leafcopy ? nv : threadIdx.x; v0 < nv; v0 += (uint64_t)blockDim.x * TU) {
       float xv[TU][8], pp[TU][2][8];
       bool okv[TU];
 #pragma unroll
@@ -844,6 +878,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+      const uint64_t ts = tr.p ? globaltimer() : 0;
       fence_acq_rel_sys();
       if (root) {
         for (int k = 0; k < nd.nchild; ++k) st_relaxed_sys(&a.pad[member(nd.child[k])]->down[lc], ep);
@@ -851,7 +886,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
       } else {
         st_relaxed_sys(&a.pad[member(nd.parent)]->up[nd.slot][lc], ep);
       }
-      tr.rec((1ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, globaltimer());
+      tr.rec((1ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, ts, globaltimer());
     }
   }
 
@@ -866,7 +901,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     if (!__syncthreads_and(got)) return;
     const uint64_t tk = tr.p ? globaltimer() : 0;
     if (nd.nchild == 0 && !PAIR) {
-      tr.rec((2ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, tk);
+      tr.rec((2ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, tk, tk);
       continue;
     }
     const uint64_t e0 = c * C, e1 = (e0 + C < len) ? e0 + C : len;
@@ -900,10 +935,11 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+      const uint64_t ts = tr.p ? globaltimer() : 0;
       fence_acq_rel_sys();
       for (int k = 0; k < nd.nchild; ++k) st_relaxed_sys(&a.pad[member(nd.child[k])]->down[lc], ep);
       if constexpr (PAIR) st_relaxed_sys(&a.pad[partner]->pdown[lc], ep);
-      tr.rec((2ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, globaltimer());
+      tr.rec((2ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, ts, globaltimer());
     }
   }
 
@@ -917,7 +953,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
         const uint64_t tw = tr.p ? globaltimer() : 0;
         wait_ge(a, &mypad->pdown[(uint32_t)(c - a.c_lo)], ep);
         const uint64_t tk = tr.p ? globaltimer() : 0;
-        tr.rec((3ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, tk);
+        tr.rec((3ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, tk, tk);
       }
     }
   }

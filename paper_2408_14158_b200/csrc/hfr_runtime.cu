@@ -1140,7 +1140,7 @@ hfr_status_t hfr_tree_query(int n, int which, int* parent, int* child0, int* chi
 
 hfr_status_t hfr_set_trace(hfr_comm_t c, void* dev_buf, size_t bytes) {
   if (!c) return HFR_ERR_NOT_INITIALIZED;
-  const size_t per = (size_t)32 * kMaxCtas * c->local;
+  const size_t per = (size_t)64 * kMaxCtas * c->local;
   if (!dev_buf || bytes < per) {
     c->trace = nullptr;
     c->trace_cap = 0;

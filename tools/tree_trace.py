@@ -4,7 +4,7 @@
   torchrun --nproc-per-node N tools/tree_trace.py --algo dbt --chunk 32768 --ctas 64 --out gpurun_out/tr
   python tools/tree_trace.py --analyze gpurun_out/tr
 
-Each rank dumps rank<r>.npy = [CTA, event, 4] u64 {tag, t_wait, t_work, t_done}
+Each rank dumps rank<r>.npy = [CTA, event, 8] u64 {tag, t_wait, t_work, t_stores_issued, t_done, ...}
 (hfr_set_trace).  The summary prints, per rank and pass, the summed wait and
 work time and the span, which tells whether a tree launch is limited by
 transfer work, by waiting on tree neighbours, or by pipeline fill/drain.
@@ -31,12 +31,12 @@ def analyze(d):
     for f in files:
         r = int(os.path.basename(f)[4:-4])
         tr = np.load(f)
-        ev = tr.reshape(-1, 4)
+        ev = tr.reshape(-1, 8)
         ev = ev[ev[:, 0] != 0]
         if ev.size == 0:
             continue
         ph = (ev[:, 0] >> 60).astype(int)
-        t0, t1, t2 = ev[:, 1].astype(np.int64), ev[:, 2].astype(np.int64), ev[:, 3].astype(np.int64)
+        t0, t1, ts, t2 = (ev[:, k].astype(np.int64) for k in (1, 2, 3, 4))
         base = t0.min()
         rep = {"span_us": (t2.max() - base) / 1e3, "events": int(len(ev))}
         for p, name in PH.items():
@@ -46,6 +46,8 @@ def analyze(d):
             rep[name] = {"n": int(m.sum()), "wait_us_sum": float((t1[m] - t0[m]).sum() / 1e3),
                          "work_us_sum": float((t2[m] - t1[m]).sum() / 1e3),
                          "work_us_mean": float((t2[m] - t1[m]).mean() / 1e3),
+                         "issue_us_mean": float((ts[m] - t1[m]).mean() / 1e3),
+                         "drain_us_mean": float((t2[m] - ts[m]).mean() / 1e3),
                          "first_done_us": float((t2[m].min() - base) / 1e3),
                          "last_done_us": float((t2[m].max() - base) / 1e3)}
         # per-CTA busy fraction
@@ -55,8 +57,8 @@ def analyze(d):
             e = tr[cta]
             e = e[e[:, 0] != 0]
             if len(e):
-                busy.append(float((e[:, 3].astype(np.int64) - e[:, 2].astype(np.int64)).sum()
-                                  / max(1, (e[:, 3].max() - e[:, 1].min()))))
+                busy.append(float((e[:, 4].astype(np.int64) - e[:, 2].astype(np.int64)).sum()
+                                  / max(1, (e[:, 4].max() - e[:, 1].min()))))
         rep["cta_busy_frac_mean"] = float(np.mean(busy)) if busy else None
         out[r] = rep
     return out
@@ -90,8 +92,8 @@ def main():
     t.normal_()
     for _ in range(3):
         comm.allreduce(t)
-    cap = 1024
-    tb = torch.zeros(32 * 1024 * cap, dtype=torch.uint8, device=f"cuda:{local}")
+    cap = 512
+    tb = torch.zeros(64 * 1024 * cap, dtype=torch.uint8, device=f"cuda:{local}")
     comm.set_trace(tb)
     dist.barrier()
     comm.barrier()
@@ -102,7 +104,7 @@ def main():
     torch.cuda.synchronize()
     comm.set_trace(None)
     os.makedirs(a.out, exist_ok=True)
-    arr = tb.view(torch.int64).view(1024, cap, 4)[: (a.ctas or 148)].cpu().numpy().view(np.uint64)
+    arr = tb.view(torch.int64).view(1024, cap, 8)[: (a.ctas or 148)].cpu().numpy().view(np.uint64)
     np.save(os.path.join(a.out, f"rank{rank}.npy"), arr)
     ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
