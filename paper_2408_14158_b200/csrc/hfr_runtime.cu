@@ -230,7 +230,6 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
 
 void resolve_defaults(hfr_config_t& c) {
   if (c.chunk_elems == 0) c.chunk_elems = 32768;
-  if (c.threads == 0) c.threads = 512;
   if (c.scratch_bytes == 0) c.scratch_bytes = 256ull << 20;
   if (c.timeout_ms == 0) c.timeout_ms = 60000;
   if (c.oneshot_max_bytes == 0) c.oneshot_max_bytes = 512u << 10;
@@ -492,10 +491,13 @@ hfr_status_t launch(hfr_comm_s* c, const void* fn, int grid_x, int threads, Args
   return HFR_SUCCESS;
 }
 
-// CTAs per rank: the config cap (default one per SM), limited so that all
-// ranks' CTAs of a virtual comm are co-resident (cooperative launch).
-hfr_status_t ctas_per_rank(hfr_comm_s* c, const void* fn, int threads, int want, int* out) {
-  int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : c->num_sms;
+// threads per CTA: the config's, else the schedule's measured best
+int cta_threads(const hfr_comm_s* c, int dflt) { return c->cfg.threads > 0 ? c->cfg.threads : dflt; }
+
+// CTAs per rank: the config cap (default `per_sm` per SM), limited so that
+// all ranks' CTAs of a virtual comm are co-resident (cooperative launch).
+hfr_status_t ctas_per_rank(hfr_comm_s* c, const void* fn, int threads, int want, int* out, int per_sm = 1) {
+  int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : per_sm * c->num_sms;
   g = std::min(g, kMaxCtas);
   if (want > 0) g = std::min(g, want);
   if (c->virt && c->local > 1) {
@@ -526,7 +528,7 @@ void base_args(hfr_comm_s* c, Args& a, uint64_t count, uint64_t sig) {
 hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                       cudaStream_t s) {
   const void* fn = dt == HFR_BFLOAT16 ? flat_fn<BF16>(c->n) : flat_fn<F32>(c->n);
-  const int threads = c->cfg.threads;
+  const int threads = cta_threads(c, 512);
   const uint64_t per = dt == HFR_BFLOAT16 ? 8 : 4;
   const uint64_t vec_per_rank = count / per / c->n + 1;
   int g = 0;
@@ -540,7 +542,9 @@ hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
 hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, bool pair, uint64_t sig,
                       cudaStream_t s) {
   const void* fn = dt == HFR_BFLOAT16 ? tree_fn<BF16>(pair) : tree_fn<F32>(pair);
-  const int threads = c->cfg.threads;
+  // 2 CTAs x 256 threads per SM: while one CTA drains its chunk's stores at
+  // the per-chunk system fence the other issues (r01: DBT n=4 377 -> 422 GB/s)
+  const int threads = cta_threads(c, 256);
   const uint64_t C = c->cfg.chunk_elems;
   Args a;
   base_args(c, a, count, 0);
@@ -573,7 +577,7 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
     // tree b & 1, so the two trees' dependency chains never interleave inside
     // one CTA (a rank is the root of one tree and a leaf of the other).
     int g = 0;
-    HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>(std::max<uint64_t>(here, 2), kMaxCtas), &g));
+    HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>(std::max<uint64_t>(here, 2), kMaxCtas), &g, 2));
     g = std::max(2, g & ~1);
     a.c_lo = (uint32_t)lo;
     a.c_hi = (uint32_t)hi;
@@ -618,7 +622,7 @@ hfr_status_t run_oneshot(hfr_comm_s* c, char* const* local_bufs, uint64_t count,
   const uint64_t nvec = count / per;
   // small grids: one CTA per 2048 vectors (32 KiB), at least n threads
   const int min_thr = 32 * ((c->n + 31) / 32);
-  const int threads = (int)std::max<uint64_t>(min_thr, std::min<uint64_t>(c->cfg.threads, round_up(std::max<uint64_t>(nvec, 1), 32)));
+  const int threads = (int)std::max<uint64_t>(min_thr, std::min<uint64_t>(cta_threads(c, 512), round_up(std::max<uint64_t>(nvec, 1), 32)));
   int g = 0;
   HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>((nvec + 2047) / 2048 + 1, kMaxCtas), &g));
   Args a;
@@ -748,7 +752,7 @@ hfr_status_t run_ce(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_
 hfr_status_t run_nvls(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig, uint64_t offset,
                       cudaStream_t s) {
   const void* fn = dt == HFR_BFLOAT16 ? (const void*)hfr_nvls_kernel<BF16> : (const void*)hfr_nvls_kernel<F32>;
-  const int threads = c->cfg.threads;
+  const int threads = cta_threads(c, 512);
   const uint64_t per = dt == HFR_BFLOAT16 ? 8 : 4;
   const uint64_t vec_per_rank = count / per / c->n + 1;
   int g = 0;
