@@ -775,10 +775,28 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     // the first add, so a CTA keeps TU x (2..4) x 32 B per thread in flight.
     constexpr int TU = 1;
     const int nchild = nd.nchild, self_pos = nd.self_pos;
-    // A DBT leaf's partial is its own x widened to fp32: stream it as a copy
-    // with 4 x 16 B in flight per thread (r01: DBT n=4 313 -> 360-378 GB/s).
+    // A DBT leaf's partial is its own x: stream it as a copy with 4 x 16 B in
+    // flight per thread (r01: DBT n=4 313 -> 360-378 GB/s).  bf16 leaves send
+    // their raw bf16 (the parent widens exactly), halving leaf traffic.
     const bool leafcopy = !PAIR && nchild == 0 && !root;
-    if (leafcopy) {
+    // slot sl of this node holds a raw-bf16 leaf partial?
+    bool slot_bf16[2] = {false, false};
+    if constexpr (!PAIR && E::kPerVec == 8) {
+      for (int sl = 0; sl < nchild; ++sl) slot_bf16[sl] = a.tree[c & 1][nd.child[sl]].nchild == 0;
+    }
+    if (leafcopy && E::kPerVec == 8) {
+      const char* srcb = mybuf + (base + e0) * 2;
+      char* dstb = reinterpret_cast<char*>(dst_part) + e0 * 2;
+      for (uint64_t q0 = threadIdx.x; q0 < nv; q0 += (uint64_t)blockDim.x * 4) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (q0 + (uint64_t)u * blockDim.x < nv) v[u] = ld128(srcb + (q0 + (uint64_t)u * blockDim.x) * 16);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (q0 + (uint64_t)u * blockDim.x < nv) st128(dstb + (q0 + (uint64_t)u * blockDim.x) * 16, v[u]);
+      }
+    } else if (leafcopy) {
       const uint64_t nq = nv * 2;  // 16 B fp32 quads
       for (uint64_t q0 = threadIdx.x; q0 < nq; q0 += (uint64_t)blockDim.x * 4) {
         float f[4][4];
@@ -821,7 +839,12 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
         }
 #pragma unroll
         for (int sl = 0; sl < 2; ++sl)
-          if (sl < nchild) load8_f32(mypart + (uint64_t)sl * a.part_stride, e, pp[u][sl]);
+          if (sl < nchild) {
+            if (E::kPerVec == 8 && slot_bf16[sl])
+              load8<E>(reinterpret_cast<const char*>(mypart + (uint64_t)sl * a.part_stride), e, pp[u][sl]);
+            else
+              load8_f32(mypart + (uint64_t)sl * a.part_stride, e, pp[u][sl]);
+          }
       }
 #pragma unroll
       for (int u = 0; u < TU; ++u) {
@@ -860,7 +883,12 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
       }
       float acc = 0.f;
       for (int k = 0; k <= nd.nchild; ++k) {
-        const float s = k == nd.self_pos ? xv : mypart[(uint64_t)(k < nd.self_pos ? k : k - 1) * a.part_stride + e];
+        float s = xv;
+        if (k != nd.self_pos) {
+          const int sl = k < nd.self_pos ? k : k - 1;
+          const float* slot = mypart + (uint64_t)sl * a.part_stride;
+          s = (E::kPerVec == 8 && slot_bf16[sl]) ? E::load1(reinterpret_cast<const char*>(slot), e) : slot[e];
+        }
         acc = k == 0 ? s : __fadd_rn(acc, s);
       }
       if (root) {
@@ -868,6 +896,8 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
         E::store1(mybuf, base + e, acc);
         for (int k = 0; k < nd.nchild; ++k) E::store1(a.buf[member(nd.child[k])], base + e, acc);
         if constexpr (PAIR) E::store1(pbuf, base + e, acc);
+      } else if (E::kPerVec == 8 && leafcopy) {
+        E::store1(reinterpret_cast<char*>(dst_part), e, acc);  // raw bf16 leaf partial (exact)
       } else {
         dst_part[e] = acc;
       }
