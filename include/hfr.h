@@ -195,6 +195,36 @@ hfr_status_t hfr_allreduce(hfr_comm_t comm, void* buf, size_t count, hfr_dtype_t
 hfr_status_t hfr_allreduce_virtual(hfr_comm_t comm, void* const* bufs, size_t count, hfr_dtype_t dtype,
                                    hfr_op_t op, hfr_stream_t stream, hfr_req_t* req);
 
+/* The other collectives HFReduce serves ("general reduce and broadcast",
+ * PAPER.md:297; FSDP/ZeRO reduce-scatter and all-gather).  All
+ * are in place on `buf` (count elements) and use the shard layout of
+ * hfr_shard_range: shard g = [lo_g, hi_g).
+ *   HFR_REDUCE_SCATTER  rank g's shard g := rank-ascending fold of shard g over all
+ *                       ranks, times scale, cast; the rest of buf is unchanged.
+ *   HFR_ALLGATHER       every rank's shard g := rank g's shard g (raw bytes, no scale).
+ *   HFR_REDUCE          root's buf := the allreduce result; other ranks' buf unchanged.
+ *   HFR_BROADCAST       every rank's buf := root's buf (raw bytes).
+ *   HFR_ALLREDUCE       = hfr_allreduce (every schedule of hfr_config_t.algo).
+ * The non-allreduce collectives always run the FLAT kernel (bit-exact, same
+ * fold order).  root is ignored except for REDUCE / BROADCAST. */
+typedef enum {
+    HFR_ALLREDUCE = 0,
+    HFR_REDUCE_SCATTER = 1,
+    HFR_ALLGATHER = 2,
+    HFR_REDUCE = 3,
+    HFR_BROADCAST = 4
+} hfr_coll_t;
+
+hfr_status_t hfr_collective(hfr_comm_t comm, hfr_coll_t coll, void* buf, size_t count, hfr_dtype_t dtype,
+                            hfr_op_t op, int root, hfr_stream_t stream, hfr_req_t* req);
+hfr_status_t hfr_collective_virtual(hfr_comm_t comm, hfr_coll_t coll, void* const* bufs, size_t count,
+                                    hfr_dtype_t dtype, hfr_op_t op, int root, hfr_stream_t stream, hfr_req_t* req);
+
+/* Host-only: shard g of a count-element buffer of dtype over nranks ranks,
+ * [*lo, *hi): 16-byte-vector granular, the ragged tail in the last shard. */
+hfr_status_t hfr_shard_range(int nranks, size_t count, hfr_dtype_t dtype, int rank, size_t* lo, size_t* hi);
+
+
 /* Complete a request.  stream != NULL: make `stream` wait for it (no host
  * block; pass (hfr_stream_t)1 = cudaStreamLegacy for the legacy default
  * stream).  stream == NULL: block the host until done and report PROTOCOL /

@@ -237,6 +237,57 @@ def fold_pairfirst(xs, chunk_elems: int, scale: float = 1.0) -> np.ndarray:
     return out
 
 
+# ----------------------------------------------------------------------------
+# The other collectives ("general reduce and broadcast", PAPER.md:297;
+# SURVEY NEXT-3).  Shard layout = reading R19.
+# ----------------------------------------------------------------------------
+
+def shard_bounds(count: int, n: int, elems_per_vec: int):
+    """Reading R19: shard g = [K*floor(V*g/n), K*floor(V*(g+1)/n)) with K the
+    elements per 16 bytes and V = floor(count/K); the last shard also takes the
+    ragged tail [K*V, count)."""
+    V = count // elems_per_vec
+    lo = [elems_per_vec * (V * g // n) for g in range(n)]
+    hi = lo[1:] + [count]
+    return list(zip(lo, hi))
+
+
+def _k(xs):
+    return 8 if xs[0].dtype == np.uint16 else 4
+
+
+def reduce_scatter(xs, scale: float = 1.0):
+    """Rank g's shard g := rank-ascending fold of shard g (Alg. 1 order),
+    scaled and cast; everything else of rank g's buffer unchanged."""
+    n = len(xs)
+    out = [x.copy() for x in xs]
+    for g, (lo, hi) in enumerate(shard_bounds(xs[0].shape[0], n, _k(xs))):
+        out[g][lo:hi] = fold_ascending([x[lo:hi] for x in xs], scale)
+    return out
+
+
+def all_gather(xs):
+    """Every rank's shard g := rank g's shard g (raw values)."""
+    n = len(xs)
+    out = [x.copy() for x in xs]
+    for g, (lo, hi) in enumerate(shard_bounds(xs[0].shape[0], n, _k(xs))):
+        for r in range(n):
+            out[r][lo:hi] = xs[g][lo:hi]
+    return out
+
+
+def reduce(xs, root: int, scale: float = 1.0):
+    """Root's buffer := the allreduce result; the others unchanged."""
+    out = [x.copy() for x in xs]
+    out[root] = fold_ascending(xs, scale)
+    return out
+
+
+def broadcast(xs, root: int):
+    """Every rank's buffer := root's buffer."""
+    return [xs[root].copy() for _ in xs]
+
+
 def allreduce(xs, algo: str = "flat", chunk_elems: int = 1 << 16, scale: float = 1.0):
     """Every rank's output (identical bytes on all ranks) for the given order."""
     if algo in ("flat", "oneshot", "auto", "ce"):

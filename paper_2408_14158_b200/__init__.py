@@ -30,6 +30,9 @@ ALGOS = {"auto": ALGO_AUTO, "flat": ALGO_FLAT, "dbt": ALGO_DBT, "pair_dbt": ALGO
          "ce": ALGO_CE, "nvls": ALGO_NVLS}
 FLOAT32, BFLOAT16 = 0, 1
 SUM = 0
+ALLREDUCE, REDUCE_SCATTER, ALLGATHER, REDUCE, BROADCAST = range(5)
+COLLS = {"allreduce": ALLREDUCE, "reduce_scatter": REDUCE_SCATTER, "allgather": ALLGATHER, "reduce": REDUCE,
+         "broadcast": BROADCAST}
 
 # every symbol include/hfr.h declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -37,7 +40,7 @@ EXPORTS = (
     "hfr_comm_local_ranks", "hfr_comm_rank", "hfr_comm_nranks", "hfr_mem_alloc", "hfr_mem_free",
     "hfr_register", "hfr_allreduce", "hfr_allreduce_virtual", "hfr_wait", "hfr_comm_status",
     "hfr_barrier", "hfr_finalize", "hfr_tree_query", "hfr_comm_launches", "hfr_status_string",
-    "hfr_last_cuda_error", "hfr_set_trace",
+    "hfr_last_cuda_error", "hfr_set_trace", "hfr_collective", "hfr_collective_virtual", "hfr_shard_range",
 )
 
 
@@ -113,6 +116,9 @@ def _lib():
             "hfr_status_string": (ctypes.c_char_p, [i]),
             "hfr_last_cuda_error": (ctypes.c_char_p, []),
             "hfr_set_trace": (i, [vp, vp, sz]),
+            "hfr_collective": (i, [vp, i, vp, sz, i, i, i, vp, p(vp)]),
+            "hfr_collective_virtual": (i, [vp, i, p(vp), sz, i, i, i, vp, p(vp)]),
+            "hfr_shard_range": (i, [i, sz, i, i, p(sz), p(sz)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -145,6 +151,14 @@ def tree_query(n: int, which: int):
     _check(_lib().hfr_tree_query(n, which, P, C0, C1), "hfr_tree_query")
     children = [[c for c in (C0[v], C1[v]) if c >= 0] for v in range(n)]
     return list(P), children
+
+
+def shard_range(nranks: int, count: int, dtype: str, rank: int):
+    """[lo, hi) of rank's shard (hfr_shard_range; dtype 'f32' or 'bf16')."""
+    lo, hi = ctypes.c_size_t(), ctypes.c_size_t()
+    code = BFLOAT16 if dtype in ("bf16", "bfloat16") else FLOAT32
+    _check(_lib().hfr_shard_range(nranks, count, code, rank, ctypes.byref(lo), ctypes.byref(hi)), "hfr_shard_range")
+    return lo.value, hi.value
 
 
 def _dtype_code(t) -> int:
@@ -335,6 +349,38 @@ class Comm:
             _check(_lib().hfr_set_trace(self._h, ctypes.c_void_p(buf.data_ptr()), buf.numel() * buf.element_size()),
                    "hfr_set_trace")
 
+    def collective(self, kind: str, tensor, root: int = 0, async_op: bool = False, stream=None) -> Optional[Work]:
+        """In-place collective (include/hfr.h hfr_collective): 'allreduce',
+        'reduce_scatter', 'allgather', 'reduce', 'broadcast'."""
+        if self.virtual:
+            raise ValueError("virtual comm: use collective_virtual(kind, list_of_tensors)")
+        if not tensor.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        req = ctypes.c_void_p()
+        st = _lib().hfr_collective(self._h, COLLS[kind], ctypes.c_void_p(tensor.data_ptr()), tensor.numel(),
+                                   _dtype_code(tensor), SUM, root, ctypes.c_void_p(_stream_handle(stream)),
+                                   ctypes.byref(req) if async_op else None)
+        _check(st, f"hfr_collective({kind})")
+        return Work(self, req, tensor) if async_op else None
+
+    def collective_virtual(self, kind: str, tensors: Sequence, root: int = 0, async_op: bool = False,
+                           stream=None) -> Optional[Work]:
+        if not self.virtual:
+            raise ValueError("not a virtual comm")
+        if len(tensors) != self.nranks:
+            raise ValueError(f"need {self.nranks} tensors")
+        t0 = tensors[0]
+        for t in tensors:
+            if t.numel() != t0.numel() or t.dtype != t0.dtype or not t.is_contiguous():
+                raise ValueError("tensors must match in numel/dtype and be contiguous")
+        ptrs = (ctypes.c_void_p * self.nranks)(*[t.data_ptr() for t in tensors])
+        req = ctypes.c_void_p()
+        st = _lib().hfr_collective_virtual(self._h, COLLS[kind], ptrs, t0.numel(), _dtype_code(t0), SUM, root,
+                                           ctypes.c_void_p(_stream_handle(stream)),
+                                           ctypes.byref(req) if async_op else None)
+        _check(st, f"hfr_collective_virtual({kind})")
+        return Work(self, req, list(tensors)) if async_op else None
+
     def barrier(self, stream=None):
         _check(_lib().hfr_barrier(self._h, ctypes.c_void_p(_stream_handle(stream))), "hfr_barrier")
 
@@ -344,4 +390,5 @@ class Comm:
             self._h = None
 
 
-__all__ = ["Comm", "Config", "Work", "HfrError", "tree_query", "status_string", "lib", "LIB_PATH", "EXPORTS"]
+__all__ = ["Comm", "Config", "Work", "HfrError", "tree_query", "shard_range", "status_string", "lib", "LIB_PATH",
+           "EXPORTS", "COLLS"]

@@ -73,6 +73,8 @@ struct Args {
   int rank0;               // rank of blockIdx.y == 0
   int chunk;               // tree chunk elements (multiple of 256)
   int ntree;               // nodes per tree (n, or n/2 for PAIR)
+  int src_rank;            // FLAT kernel: -1 fold all ranks; -2 copy my own shard; r>=0 copy rank r's
+  uint32_t dst_mask;       // FLAT kernel: ranks that receive the result (0 = the owner itself)
   char* mcbuf;              // NVLS: multicast VA of this call's buffer
   uint32_t* mc_exit;       // NVLS: multicast VA of the exit counters [kMaxCtas]
   uint32_t* uc_exit;       // NVLS: local unicast VA of the same counters
@@ -300,14 +302,29 @@ struct BF16 {
 // shard g of rank q's buffer is read and then written only by rank g.
 // ---------------------------------------------------------------------------
 template <class E, int NR, int U>
-__device__ __forceinline__ void flat_vecs(const Args& a, uint64_t i, uint64_t stride, uint64_t hi) {
-  // U vectors per thread, all U*NR loads issued before the first fold so that
-  // U*NR 16-byte NVLink reads are in flight per thread.
+__device__ __forceinline__ void flat_vecs(const Args& a, uint64_t i, uint64_t stride, uint64_t hi, int src,
+                                          uint32_t dmask) {
+  // U vectors per thread, all loads issued before the first fold so that
+  // U*NR 16-byte NVLink reads are in flight per thread.  src >= 0: copy that
+  // rank's vectors (all-gather / broadcast) instead of folding all ranks.
   constexpr int K = E::kPerVec;
   uint4 v[U][NR];
   bool ok[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) ok[u] = i + u * stride < hi;
+  if (src >= 0) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) v[u][0] = ld128(a.buf[src] + (i + u * stride) * 16);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (ok[u]) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+          if ((dmask >> r) & 1u) st128(a.buf[r] + (i + u * stride) * 16, v[u][0]);
+      }
+    return;
+  }
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     if (ok[u]) {
@@ -331,14 +348,21 @@ __device__ __forceinline__ void flat_vecs(const Args& a, uint64_t i, uint64_t st
       for (int k = 0; k < K; ++k) acc[k] = __fmul_rn(acc[k], a.scale);
       const uint4 o = E::narrow(acc);
 #pragma unroll
-      for (int r = 0; r < NR; ++r) st128(a.buf[r] + (i + u * stride) * 16, o);
+      for (int r = 0; r < NR; ++r)
+        if ((dmask >> r) & 1u) st128(a.buf[r] + (i + u * stride) * 16, o);
     }
   }
 }
 
 template <class E>
-__device__ __forceinline__ void flat_vec_dyn(const Args& a, const int n, uint64_t i) {
+__device__ __forceinline__ void flat_vec_dyn(const Args& a, const int n, uint64_t i, int src, uint32_t dmask) {
   constexpr int K = E::kPerVec;
+  if (src >= 0) {
+    const uint4 o = ld128(a.buf[src] + i * 16);
+    for (int r = 0; r < n; ++r)
+      if ((dmask >> r) & 1u) st128(a.buf[r] + i * 16, o);
+    return;
+  }
   float acc[K];
   E::widen(ld128(a.buf[0] + i * 16), acc);
   for (int r = 1; r < n; ++r) {
@@ -350,7 +374,8 @@ __device__ __forceinline__ void flat_vec_dyn(const Args& a, const int n, uint64_
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = __fmul_rn(acc[k], a.scale);
   const uint4 o = E::narrow(acc);
-  for (int r = 0; r < n; ++r) st128(a.buf[r] + i * 16, o);
+  for (int r = 0; r < n; ++r)
+    if ((dmask >> r) & 1u) st128(a.buf[r] + i * 16, o);
 }
 
 // NR = compile-time rank count (1..8), 0 = runtime a.n (up to kMaxRanks).
@@ -360,6 +385,11 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
   const int n = NR > 0 ? NR : a.n;
   const int b = blockIdx.x;
   const uint64_t e = begin_epoch(a.pad[rank]);
+  // collective mode (NEXT-3): allreduce = fold all -> all; reduce-scatter =
+  // fold all -> owner; reduce = fold all -> root; all-gather = owner's shard
+  // -> all; broadcast = root's shard -> all
+  const int src = a.src_rank == -2 ? rank : a.src_rank;
+  const uint32_t dmask = a.dst_mask ? a.dst_mask : (1u << rank);
   if (entry_barrier(a, rank, b, e)) {
     constexpr int K = E::kPerVec;
     constexpr int U = NR > 4 ? 2 : (NR > 2 ? 3 : 4);
@@ -374,19 +404,33 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
       const uint64_t warps = stride / 32;
       const uint64_t w = ((uint64_t)b * blockDim.x + threadIdx.x) / 32;
       for (uint64_t t0 = lo + w * (U * 32); t0 < hi; t0 += warps * (U * 32))
-        flat_vecs<E, NR, U>(a, t0 + lane, 32, hi);
+        flat_vecs<E, NR, U>(a, t0 + lane, 32, hi, src, dmask);
     } else {
       for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += stride)
-        flat_vec_dyn<E>(a, n, i);
+        flat_vec_dyn<E>(a, n, i, src, dmask);
     }
     // ragged tail (< K elements) — owned by the last rank, CTA 0
     const uint64_t t0 = nvec * K;
     if (rank == n - 1 && b == 0 && threadIdx.x < a.count - t0) {
       const uint64_t el = t0 + threadIdx.x;
-      float acc = E::load1(a.buf[0], el);
-      for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, E::load1(a.buf[r], el));
-      acc = __fmul_rn(acc, a.scale);
-      for (int r = 0; r < n; ++r) E::store1(a.buf[r], el, acc);
+      if (src >= 0) {
+        // raw copy of the element (bf16 bits or fp32 bits)
+        if constexpr (K == 8) {
+          const uint16_t x = reinterpret_cast<const uint16_t*>(a.buf[src])[el];
+          for (int r = 0; r < n; ++r)
+            if ((dmask >> r) & 1u) reinterpret_cast<uint16_t*>(a.buf[r])[el] = x;
+        } else {
+          const uint32_t x = reinterpret_cast<const uint32_t*>(a.buf[src])[el];
+          for (int r = 0; r < n; ++r)
+            if ((dmask >> r) & 1u) reinterpret_cast<uint32_t*>(a.buf[r])[el] = x;
+        }
+      } else {
+        float acc = E::load1(a.buf[0], el);
+        for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, E::load1(a.buf[r], el));
+        acc = __fmul_rn(acc, a.scale);
+        for (int r = 0; r < n; ++r)
+          if ((dmask >> r) & 1u) E::store1(a.buf[r], el, acc);
+      }
     }
   }
   exit_barrier(a, rank, b, e);

@@ -523,10 +523,26 @@ void base_args(hfr_comm_s* c, Args& a, uint64_t count, uint64_t sig) {
   a.rank0 = c->virt ? 0 : c->rank;
   a.trace = c->trace;
   a.trace_cap = c->trace_cap;
+  a.src_rank = -1;  // fold all ranks ...
+  a.dst_mask = c->n >= 32 ? ~0u : ((1u << c->n) - 1);  // ... into every rank (allreduce)
+}
+
+// FLAT-kernel routing of a collective (NEXT-3, "general reduce
+// and broadcast"): which rank's shard is read (-1: fold all, -2: my own) and
+// which ranks receive it (0: the shard's owner).
+void coll_routing(const hfr_comm_s* c, int coll, int root, int* src, uint32_t* dmask) {
+  const uint32_t all = c->n >= 32 ? ~0u : ((1u << c->n) - 1);
+  switch (coll) {
+    case HFR_REDUCE_SCATTER: *src = -1; *dmask = 0; break;
+    case HFR_ALLGATHER: *src = -2; *dmask = all; break;
+    case HFR_REDUCE: *src = -1; *dmask = 1u << root; break;
+    case HFR_BROADCAST: *src = root; *dmask = all & ~(1u << root); break;
+    default: *src = -1; *dmask = all;
+  }
 }
 
 hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
-                      cudaStream_t s) {
+                      cudaStream_t s, int coll = HFR_ALLREDUCE, int root = 0) {
   const void* fn = dt == HFR_BFLOAT16 ? flat_fn<BF16>(c->n) : flat_fn<F32>(c->n);
   const int threads = cta_threads(c, 512);
   const uint64_t per = dt == HFR_BFLOAT16 ? 8 : 4;
@@ -536,6 +552,7 @@ hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   Args a;
   base_args(c, a, count, fnv(sig, (uint64_t)g * 1315423911ull + threads));
   for (int q = 0; q < c->n; ++q) a.buf[q] = bufs[q];
+  coll_routing(c, coll, root, &a.src_rank, &a.dst_mask);
   return launch(c, fn, g, threads, a, s);
 }
 
@@ -806,13 +823,16 @@ cudaEvent_t take_event(hfr_comm_s* c) {
 // The body shared by hfr_allreduce / hfr_allreduce_virtual.  bufs[q] is local
 // rank q's buffer (virtual: q = 0..n-1; real: only bufs[0] = this rank's).
 hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count, hfr_dtype_t dt, hfr_op_t op,
-                            cudaStream_t user, hfr_req_t* req) {
+                            cudaStream_t user, hfr_req_t* req, int coll = HFR_ALLREDUCE, int root = 0) {
   if (!c) return HFR_ERR_NOT_INITIALIZED;
   if (req) *req = nullptr;
   if (dt != HFR_FLOAT32 && dt != HFR_BFLOAT16) return HFR_ERR_INVALID_ARGUMENT;
+  if (coll < HFR_ALLREDUCE || coll > HFR_BROADCAST) return HFR_ERR_INVALID_ARGUMENT;
+  if ((coll == HFR_REDUCE || coll == HFR_BROADCAST) && (root < 0 || root >= c->n)) return HFR_ERR_INVALID_ARGUMENT;
   if (op != HFR_SUM) return HFR_ERR_UNSUPPORTED;
   if (c->sticky != HFR_SUCCESS) return c->sticky;
-  const int algo = effective_algo(c, count * dtype_size(dt));
+  // the other collectives run on the FLAT kernel's routing (NEXT-3)
+  const int algo = coll == HFR_ALLREDUCE ? effective_algo(c, count * dtype_size(dt)) : HFR_ALGO_FLAT;
   if (algo == HFR_ALGO_PAIR_DBT && c->n % 2 != 0) return HFR_ERR_UNSUPPORTED;
   if (algo == HFR_ALGO_NVLS && (c->virt || !c->nvls || !c->nvls->on)) return HFR_ERR_UNSUPPORTED;
   for (int q = 0; q < c->local; ++q)
@@ -853,7 +873,8 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     HFR_TRY(ensure_scratch(c, scratch_need(c, count, dt, algo)));
     uint64_t sig = 1469598103934665603ull;
     sig = fnv(sig, count);
-    sig = fnv(sig, (uint64_t)dt | ((uint64_t)op << 8) | ((uint64_t)algo << 16));
+    sig = fnv(sig, (uint64_t)dt | ((uint64_t)op << 8) | ((uint64_t)algo << 16) | ((uint64_t)coll << 24) |
+                       ((uint64_t)root << 32));
     uint32_t sbits;
     memcpy(&sbits, &c->cfg.scale, 4);
     sig = fnv(sig, sbits);
@@ -884,7 +905,7 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     } else if (algo == HFR_ALGO_CE && zero_copy) {
       HFR_TRY(run_ce(c, bufs, count, dt, s));
     } else if (algo == HFR_ALGO_FLAT || algo == HFR_ALGO_CE) {
-      HFR_TRY(run_flat(c, bufs, count, dt, sig, s));
+      HFR_TRY(run_flat(c, bufs, count, dt, sig, s, coll, root));
     } else {
       HFR_TRY(run_tree(c, bufs, count, dt, algo == HFR_ALGO_PAIR_DBT, sig, s));
     }
@@ -1059,6 +1080,34 @@ hfr_status_t hfr_allreduce_virtual(hfr_comm_t c, void* const* bufs, size_t count
   char* local[kMaxRanks];
   for (int q = 0; q < c->n; ++q) local[q] = (char*)bufs[q];
   return allreduce_impl(c, local, count, dtype, op, (cudaStream_t)stream, req);
+}
+
+hfr_status_t hfr_collective(hfr_comm_t c, hfr_coll_t coll, void* buf, size_t count, hfr_dtype_t dtype, hfr_op_t op,
+                            int root, hfr_stream_t stream, hfr_req_t* req) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  if (c->virt) return HFR_ERR_INVALID_ARGUMENT;
+  char* bufs[1] = {(char*)buf};
+  return allreduce_impl(c, bufs, count, dtype, op, (cudaStream_t)stream, req, coll, root);
+}
+
+hfr_status_t hfr_collective_virtual(hfr_comm_t c, hfr_coll_t coll, void* const* bufs, size_t count,
+                                    hfr_dtype_t dtype, hfr_op_t op, int root, hfr_stream_t stream, hfr_req_t* req) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  if (!c->virt || !bufs) return HFR_ERR_INVALID_ARGUMENT;
+  char* local[kMaxRanks];
+  for (int q = 0; q < c->n; ++q) local[q] = (char*)bufs[q];
+  return allreduce_impl(c, local, count, dtype, op, (cudaStream_t)stream, req, coll, root);
+}
+
+hfr_status_t hfr_shard_range(int nranks, size_t count, hfr_dtype_t dtype, int rank, size_t* lo, size_t* hi) {
+  if (nranks < 1 || nranks > HFR_MAX_RANKS || rank < 0 || rank >= nranks || !lo || !hi ||
+      (dtype != HFR_FLOAT32 && dtype != HFR_BFLOAT16))
+    return HFR_ERR_INVALID_ARGUMENT;
+  const uint64_t K = dtype == HFR_BFLOAT16 ? 8 : 4;  // elements per 16-byte vector
+  const uint64_t nvec = count / K;
+  *lo = K * (nvec * (uint64_t)rank / nranks);
+  *hi = rank == nranks - 1 ? count : K * (nvec * (uint64_t)(rank + 1) / nranks);
+  return HFR_SUCCESS;
 }
 
 hfr_status_t hfr_wait(hfr_req_t req, hfr_stream_t stream) {

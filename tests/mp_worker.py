@@ -90,6 +90,23 @@ def gpu_cases(rank, world, port, outdir):
             res["ok"].append("ddp")
         except AssertionError as e:
             res["fail"].append(str(e)[:500])
+        # the other collectives (NEXT-3), one rank per GPU
+        comm.set_config(hfr.Config(scale=0.5))
+        for kind in ("reduce_scatter", "allgather", "reduce", "broadcast"):
+            for dtype in (gen.FP32, gen.BF16):
+                N = 200_003
+                xs = gen.rank_inputs(world, N, dtype, "normal", seed_base=6000 + N)
+                t = comm.empty(N, torch_dtype(dtype))
+                t.copy_(to_torch(xs[rank], t.device))
+                comm.collective(kind, t, root=1)
+                torch.cuda.synchronize()
+                want = {"reduce_scatter": lambda: O.reduce_scatter(xs, 0.5), "allgather": lambda: O.all_gather(xs),
+                        "reduce": lambda: O.reduce(xs, 1, 0.5), "broadcast": lambda: O.broadcast(xs, 1)}[kind]()
+                try:
+                    assert_bit_exact(to_numpy(t), want[rank], f"{kind}/{dtype}")
+                    res["ok"].append(f"{kind}/{dtype}")
+                except AssertionError as e:
+                    res["fail"].append(str(e)[:500])
         # protocol mismatch: different counts (same grid) -> PROTOCOL on every rank
         comm.set_config(hfr.Config(algo="flat"))
         t = comm.empty(8192, torch.float32)

@@ -196,3 +196,27 @@ def test_cuda_graph_replay(hfr, algo, N):
     torch.cuda.synchronize()
     assert comm.status() == hfr.SUCCESS
     check([to_numpy(b) for b in bufs], want[0], f"graph {algo}")
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16])
+@pytest.mark.parametrize("kind", ["reduce_scatter", "allgather", "reduce", "broadcast", "allreduce"])
+@pytest.mark.parametrize("N", [5, 4096 + 13, 300_007])
+def test_collectives(hfr, n, dtype, kind, N):
+    """NEXT-3: the other collectives, bit-exact vs the oracle (whole buffers,
+    including the parts a collective must leave unchanged)."""
+    comm = comm_for(hfr, n)
+    comm.set_config(hfr.Config(scale=0.5))
+    root = n - 1
+    xs = gen.rank_inputs(n, N, dtype, "normal", seed_base=300 + N)
+    bufs = comm.empty(N, torch_dtype(dtype))
+    for b, x in zip(bufs, xs):
+        b.copy_(to_torch(x, "cuda:0"))
+    comm.collective_virtual(kind, bufs, root=root)
+    torch.cuda.synchronize()
+    assert comm.status() == hfr.SUCCESS
+    want = {"reduce_scatter": lambda: O.reduce_scatter(xs, 0.5), "allgather": lambda: O.all_gather(xs),
+            "reduce": lambda: O.reduce(xs, root, 0.5), "broadcast": lambda: O.broadcast(xs, root),
+            "allreduce": lambda: O.allreduce(xs, "flat", scale=0.5)}[kind]()
+    for r, b in enumerate(bufs):
+        assert_bit_exact(to_numpy(b), want[r], f"{kind} n={n} rank {r}")
