@@ -34,6 +34,8 @@ def main():
     p.add_argument("--nccl", action="store_true")
     p.add_argument("--graph", action="store_true", help="time `iters` calls captured in one CUDA graph")
     p.add_argument("--nvls", type=int, default=0, help="NVLS arena bytes per rank (enables algo nvls)")
+    p.add_argument("--coll", default="allreduce", choices=["allreduce", "reduce_scatter", "allgather", "reduce",
+                                                             "broadcast"])
     p.add_argument("--out", default="")
     a = p.parse_args()
 
@@ -112,6 +114,10 @@ def main():
                 out.write(s + "\n")
                 out.flush()
 
+    # nccl-tests bus-bandwidth factors
+    fac = {"allreduce": 2.0 * (n - 1) / n, "reduce_scatter": (n - 1) / n, "allgather": (n - 1) / n,
+           "reduce": 1.0, "broadcast": 1.0}[a.coll]
+
     for size in sizes:
         cnt = size // esz
         views = [b[:cnt] for b in bufs]
@@ -125,21 +131,27 @@ def main():
             if algo == "barrier":   # handshake latency only (hfr_barrier kernel)
                 fn = lambda: comm.barrier(torch.cuda.current_stream())  # noqa: E731
             elif multi:
-                fn = lambda: comm.allreduce(views[0])  # noqa: E731
+                fn = lambda: comm.collective(a.coll, views[0])  # noqa: E731
             else:
-                fn = lambda: comm.allreduce_virtual(views)  # noqa: E731
+                fn = lambda: comm.collective_virtual(a.coll, views)  # noqa: E731
             t = timeit(fn, iters)
             st = comm.status()
             if st != hfr.SUCCESS:
                 raise SystemExit(f"hfr error {hfr.status_string(st)}")
-            emit({"impl": "hfr", "n": n, "virtual": not multi, "graph": a.graph, "dtype": a.dtype, "bytes": size, "algo": algo,
-                  "chunk": chunk, "ctas": ctas, "threads": thr, "us": t * 1e6,
-                  "busbw": size / t * 2 * (n - 1) / n / 1e9, "algbw": size / t / 1e9})
+            emit({"impl": "hfr", "coll": a.coll, "n": n, "virtual": not multi, "graph": a.graph, "dtype": a.dtype,
+                  "bytes": size, "algo": algo, "chunk": chunk, "ctas": ctas, "threads": thr, "us": t * 1e6,
+                  "busbw": size / t * fac / 1e9, "algbw": size / t / 1e9})
         if multi and a.nccl:
             t_ = torch.empty(cnt, dtype=tdt, device=dev).normal_()
-            tn = timeit(lambda: dist.all_reduce(t_), iters)
-            emit({"impl": "nccl", "n": n, "graph": a.graph, "dtype": a.dtype, "bytes": size, "us": tn * 1e6,
-                  "busbw": size / tn * 2 * (n - 1) / n / 1e9, "algbw": size / tn / 1e9,
+            o_ = torch.empty(cnt // n, dtype=tdt, device=dev)
+            nfn = {"allreduce": lambda: dist.all_reduce(t_),
+                   "reduce_scatter": lambda: dist.reduce_scatter_tensor(o_, t_[: o_.numel() * n]),
+                   "allgather": lambda: dist.all_gather_into_tensor(t_[: o_.numel() * n], o_),
+                   "reduce": lambda: dist.reduce(t_, 0),
+                   "broadcast": lambda: dist.broadcast(t_, 0)}[a.coll]
+            tn = timeit(nfn, iters)
+            emit({"impl": "nccl", "coll": a.coll, "n": n, "graph": a.graph, "dtype": a.dtype, "bytes": size,
+                  "us": tn * 1e6, "busbw": size / tn * fac / 1e9, "algbw": size / tn / 1e9,
                   "env": {k: v for k, v in os.environ.items() if k.startswith("NCCL_")}})
             del t_
     comm.finalize()
