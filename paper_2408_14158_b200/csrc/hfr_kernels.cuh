@@ -75,6 +75,7 @@ struct Args {
   int ntree;               // nodes per tree (n, or n/2 for PAIR)
   int src_rank;            // FLAT kernel: -1 fold all ranks; -2 copy my own shard; r>=0 copy rank r's
   uint32_t dst_mask;       // FLAT kernel: ranks that receive the result (0 = the owner itself)
+  int excl_root;           // FLAT kernel: >= 0: this rank owns no shard (reduce/broadcast root)
   char* mcbuf;              // NVLS: multicast VA of this call's buffer
   uint32_t* mc_exit;       // NVLS: multicast VA of the exit counters [kMaxCtas]
   uint32_t* uc_exit;       // NVLS: local unicast VA of the same counters
@@ -390,11 +391,16 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
   // -> all; broadcast = root's shard -> all
   const int src = a.src_rank == -2 ? rank : a.src_rank;
   const uint32_t dmask = a.dst_mask ? a.dst_mask : (1u << rank);
-  if (entry_barrier(a, rank, b, e)) {
+  // shard owners: all n ranks, or (reduce / broadcast) the n-1 ranks other
+  // than the root, so the root's link carries each byte once
+  const int nown = a.excl_root >= 0 ? n - 1 : n;
+  const int own = a.excl_root >= 0 ? (rank < a.excl_root ? rank : rank - 1) : rank;
+  const bool owner = rank != a.excl_root;
+  if (entry_barrier(a, rank, b, e) && owner) {
     constexpr int K = E::kPerVec;
     constexpr int U = NR > 4 ? 2 : (NR > 2 ? 3 : 4);
     const uint64_t nvec = a.count / K;
-    const uint64_t lo = nvec * rank / n, hi = nvec * (rank + 1) / n;
+    const uint64_t lo = nvec * own / nown, hi = nvec * (own + 1) / nown;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     if constexpr (NR > 0) {
       // warp tiles of U*32 consecutive vectors (U*512 B contiguous per rank
@@ -409,9 +415,9 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
       for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += stride)
         flat_vec_dyn<E>(a, n, i, src, dmask);
     }
-    // ragged tail (< K elements) — owned by the last rank, CTA 0
+    // ragged tail (< K elements) — owned by the last owner, CTA 0
     const uint64_t t0 = nvec * K;
-    if (rank == n - 1 && b == 0 && threadIdx.x < a.count - t0) {
+    if (own == nown - 1 && b == 0 && threadIdx.x < a.count - t0) {
       const uint64_t el = t0 + threadIdx.x;
       if (src >= 0) {
         // raw copy of the element (bf16 bits or fp32 bits)

@@ -525,12 +525,14 @@ void base_args(hfr_comm_s* c, Args& a, uint64_t count, uint64_t sig) {
   a.trace_cap = c->trace_cap;
   a.src_rank = -1;  // fold all ranks ...
   a.dst_mask = c->n >= 32 ? ~0u : ((1u << c->n) - 1);  // ... into every rank (allreduce)
+  a.excl_root = -1;
 }
 
 // FLAT-kernel routing of a collective (NEXT-3, "general reduce
 // and broadcast"): which rank's shard is read (-1: fold all, -2: my own) and
 // which ranks receive it (0: the shard's owner).
-void coll_routing(const hfr_comm_s* c, int coll, int root, int* src, uint32_t* dmask) {
+void coll_routing(const hfr_comm_s* c, int coll, int root, int* src, uint32_t* dmask, int* excl) {
+  *excl = (coll == HFR_REDUCE || coll == HFR_BROADCAST) && c->n > 1 ? root : -1;
   const uint32_t all = c->n >= 32 ? ~0u : ((1u << c->n) - 1);
   switch (coll) {
     case HFR_REDUCE_SCATTER: *src = -1; *dmask = 0; break;
@@ -552,7 +554,7 @@ hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   Args a;
   base_args(c, a, count, fnv(sig, (uint64_t)g * 1315423911ull + threads));
   for (int q = 0; q < c->n; ++q) a.buf[q] = bufs[q];
-  coll_routing(c, coll, root, &a.src_rank, &a.dst_mask);
+  coll_routing(c, coll, root, &a.src_rank, &a.dst_mask, &a.excl_root);
   return launch(c, fn, g, threads, a, s);
 }
 
