@@ -6,9 +6,10 @@ DESIGN.md §"Input recipe" lists. Both the oracle (oracle/) and the CUDA path
 (paper_2408_14158_b200/) consume these arrays; neither side imports the other.
 
 Dtype encoding: fp32 buffers are ``np.float32`` arrays; bf16 buffers are
-``np.uint16`` arrays holding the raw bfloat16 bit patterns.  bf16 values are
-obtained by TRUNCATING a float32 draw to its top 16 bits (round-toward-zero
-bit slicing), which is input generation, not the method's RNE cast.
+``np.uint16`` arrays holding the raw bfloat16 bit patterns; fp16 buffers are
+``np.float16``.  bf16 values are obtained by TRUNCATING a float32 draw to its
+top 16 bits (round-toward-zero bit slicing); fp16 values by numpy's
+float32 -> float16 conversion of the draw (input generation only).
 
 Seeds follow SURVEY.md §8d: ``np.random.default_rng(base + rank)``.
 """
@@ -18,6 +19,7 @@ import numpy as np
 
 FP32 = "f32"
 BF16 = "bf16"
+FP16 = "f16"
 
 # Distribution names:
 #   normal     N(0, 1)
@@ -35,7 +37,7 @@ def _draw_f32(rng: np.random.Generator, dist: str, count: int, dtype: str) -> np
     if dist == "grad":
         return (rng.standard_normal(count, dtype=np.float32) * np.float32(1e-3)).astype(np.float32)
     if dist == "int":
-        lim = (1 << 20) - 1 if dtype == FP32 else 256
+        lim = (1 << 20) - 1 if dtype == FP32 else 256  # bf16/fp16: exact, sums exact in fp32
         return rng.integers(-lim, lim + 1, size=count, dtype=np.int64).astype(np.float32)
     if dist == "loguniform":
         e = rng.uniform(-20.0, 4.0, size=count)
@@ -61,6 +63,9 @@ def _to_dtype(x: np.ndarray, dtype: str) -> np.ndarray:
         return np.ascontiguousarray(x, dtype=np.float32)
     if dtype == BF16:
         return (np.ascontiguousarray(x, dtype=np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    if dtype == FP16:
+        with np.errstate(over="ignore"):
+            return np.ascontiguousarray(x, dtype=np.float32).astype(np.float16)
     raise ValueError(f"unknown dtype {dtype!r}")
 
 

@@ -33,9 +33,10 @@ typedef struct hfr_comm_s* hfr_comm_t;
 typedef struct hfr_req_s* hfr_req_t;
 typedef void* hfr_stream_t; /* cudaStream_t */
 
-/* Element types.  bf16 is reduced with fp32 accumulation and ONE final RNE
- * rounding (reading R2; PAPER.md:404 lists FP32/FP16/BF16/FP8). */
-typedef enum { HFR_FLOAT32 = 0, HFR_BFLOAT16 = 1 } hfr_dtype_t;
+/* Element types.  bf16 and fp16 are reduced with fp32 accumulation and ONE
+ * final RNE rounding (reading R2; PAPER.md:404 lists
+ * FP32/FP16/BF16/FP8). */
+typedef enum { HFR_FLOAT32 = 0, HFR_BFLOAT16 = 1, HFR_FLOAT16 = 2 } hfr_dtype_t;
 
 /* Reduction operator.  The paper's only operator is the sum ("reduction add
  * operation"). */

@@ -31,6 +31,7 @@ import numpy as np
 
 F32 = "f32"
 BF16 = "bf16"
+F16 = "f16"
 
 PAIR_SPLIT_ALIGN = 256  # elements; reading R13 (half boundary alignment)
 
@@ -40,11 +41,14 @@ PAIR_SPLIT_ALIGN = 256  # elements; reading R13 (half boundary alignment)
 # ----------------------------------------------------------------------------
 
 def widen(x: np.ndarray) -> np.ndarray:
-    """Exact widening to fp32: bf16 bit patterns -> float32 (upper 16 bits)."""
+    """Exact widening to fp32: bf16 bit patterns -> float32 (upper 16 bits);
+    IEEE binary16 -> float32 (every half is a float)."""
     if x.dtype == np.float32:
         return x
     if x.dtype == np.uint16:
         return (x.astype(np.uint32) << np.uint32(16)).view(np.float32)
+    if x.dtype == np.float16:
+        return x.astype(np.float32)
     raise TypeError(f"unsupported oracle dtype {x.dtype}")
 
 
@@ -74,11 +78,21 @@ def _finish(acc: np.ndarray, scale: float, out_dtype: str) -> np.ndarray:
         return y
     if out_dtype == BF16:
         return bf16_rne(y)
+    if out_dtype == F16:
+        return y.astype(np.float16)  # numpy's float32 -> binary16 conversion rounds to nearest even
     raise ValueError(out_dtype)
 
 
 def _out_dtype(xs) -> str:
-    return BF16 if xs[0].dtype == np.uint16 else F32
+    if xs[0].dtype == np.uint16:
+        return BF16
+    if xs[0].dtype == np.float16:
+        return F16
+    return F32
+
+
+def _out_np(out_dtype: str):
+    return {F32: np.float32, BF16: np.uint16, F16: np.float16}[out_dtype]
 
 
 # ----------------------------------------------------------------------------
@@ -190,7 +204,7 @@ def fold_tree(xs, chunk_elems: int, scale: float = 1.0) -> np.ndarray:
     count = xs[0].shape[0]
     trees = build_double_binary_tree(n)
     out_dtype = _out_dtype(xs)
-    out = np.empty(count, dtype=np.float32 if out_dtype == F32 else np.uint16)
+    out = np.empty(count, dtype=_out_np(out_dtype))
     for c0 in range(0, count, chunk_elems):
         c = c0 // chunk_elems
         sl = slice(c0, min(c0 + chunk_elems, count))
@@ -224,7 +238,7 @@ def fold_pairfirst(xs, chunk_elems: int, scale: float = 1.0) -> np.ndarray:
     m = n // 2
     trees = build_double_binary_tree(m)
     out_dtype = _out_dtype(xs)
-    out = np.empty(count, dtype=np.float32 if out_dtype == F32 else np.uint16)
+    out = np.empty(count, dtype=_out_np(out_dtype))
     H = pair_split(count)
     for lo, hi in ((0, H), (H, count)):
         for c0 in range(lo, hi, chunk_elems):
@@ -253,7 +267,7 @@ def shard_bounds(count: int, n: int, elems_per_vec: int):
 
 
 def _k(xs):
-    return 8 if xs[0].dtype == np.uint16 else 4
+    return 4 if xs[0].dtype == np.float32 else 8
 
 
 def reduce_scatter(xs, scale: float = 1.0):

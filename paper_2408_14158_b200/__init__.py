@@ -28,7 +28,7 @@ SUCCESS, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED, ERR_CUDA, ERR_OUT_OF_MEMORY, ERR
 ALGO_AUTO, ALGO_FLAT, ALGO_DBT, ALGO_PAIR_DBT, ALGO_ONESHOT, ALGO_CE, ALGO_NVLS = range(7)
 ALGOS = {"auto": ALGO_AUTO, "flat": ALGO_FLAT, "dbt": ALGO_DBT, "pair_dbt": ALGO_PAIR_DBT, "oneshot": ALGO_ONESHOT,
          "ce": ALGO_CE, "nvls": ALGO_NVLS}
-FLOAT32, BFLOAT16 = 0, 1
+FLOAT32, BFLOAT16, FLOAT16 = 0, 1, 2
 SUM = 0
 ALLREDUCE, REDUCE_SCATTER, ALLGATHER, REDUCE, BROADCAST = range(5)
 COLLS = {"allreduce": ALLREDUCE, "reduce_scatter": REDUCE_SCATTER, "allgather": ALLGATHER, "reduce": REDUCE,
@@ -156,7 +156,7 @@ def tree_query(n: int, which: int):
 def shard_range(nranks: int, count: int, dtype: str, rank: int):
     """[lo, hi) of rank's shard (hfr_shard_range; dtype 'f32' or 'bf16')."""
     lo, hi = ctypes.c_size_t(), ctypes.c_size_t()
-    code = BFLOAT16 if dtype in ("bf16", "bfloat16") else FLOAT32
+    code = {"bf16": BFLOAT16, "bfloat16": BFLOAT16, "f16": FLOAT16, "float16": FLOAT16}.get(dtype, FLOAT32)
     _check(_lib().hfr_shard_range(nranks, count, code, rank, ctypes.byref(lo), ctypes.byref(hi)), "hfr_shard_range")
     return lo.value, hi.value
 
@@ -167,7 +167,9 @@ def _dtype_code(t) -> int:
         return FLOAT32
     if t.dtype == torch.bfloat16:
         return BFLOAT16
-    raise TypeError(f"hfr supports float32 and bfloat16, not {t.dtype}")
+    if t.dtype == torch.float16:
+        return FLOAT16
+    raise TypeError(f"hfr supports float32, bfloat16 and float16, not {t.dtype}")
 
 
 def _stream_handle(stream) -> int:

@@ -14,7 +14,10 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
+
+#include <type_traits>
 
 namespace hfr {
 
@@ -262,6 +265,7 @@ struct F32 {
   __device__ static __forceinline__ void store1(char* p, uint64_t i, float v) {
     reinterpret_cast<float*>(p)[i] = v;
   }
+  __device__ static __forceinline__ float from_bits(uint32_t b) { return __uint_as_float(b); }
 };
 
 struct BF16 {
@@ -288,6 +292,35 @@ struct BF16 {
   __device__ static __forceinline__ void store1(char* p, uint64_t i, float v) {
     reinterpret_cast<uint16_t*>(p)[i] = (uint16_t)rne(v);
   }
+  __device__ static __forceinline__ float from_bits(uint32_t b) { return __uint_as_float(b << 16); }
+};
+
+// IEEE binary16 (PAPER.md:404 lists FP16): widened exactly, fp32 accumulate,
+// one RNE rounding (__float2half_rn: subnormals kept, overflow -> Inf).
+struct F16 {
+  using T = __half;
+  static constexpr int kPerVec = 8;
+  __device__ static __forceinline__ float h2f(uint32_t b) { return __half2float(__ushort_as_half((unsigned short)b)); }
+  __device__ static __forceinline__ void widen(const uint4& v, float* f) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      f[2 * j] = h2f(w[j] & 0xFFFFu);
+      f[2 * j + 1] = h2f(w[j] >> 16);
+    }
+  }
+  __device__ static __forceinline__ uint32_t rne(float x) { return (uint32_t)__half_as_ushort(__float2half_rn(x)); }
+  __device__ static __forceinline__ uint4 narrow(const float* f) {
+    return make_uint4(rne(f[0]) | (rne(f[1]) << 16), rne(f[2]) | (rne(f[3]) << 16),
+                      rne(f[4]) | (rne(f[5]) << 16), rne(f[6]) | (rne(f[7]) << 16));
+  }
+  __device__ static __forceinline__ float load1(const char* p, uint64_t i) {
+    return h2f(reinterpret_cast<const uint16_t*>(p)[i]);
+  }
+  __device__ static __forceinline__ void store1(char* p, uint64_t i, float v) {
+    reinterpret_cast<uint16_t*>(p)[i] = (uint16_t)rne(v);
+  }
+  __device__ static __forceinline__ float from_bits(uint32_t b) { return h2f(b); }
 };
 
 // ---------------------------------------------------------------------------
@@ -547,8 +580,7 @@ __device__ __forceinline__ uint32_t elem_bits(const char* p, uint64_t e) {
 }
 template <class E>
 __device__ __forceinline__ float bits_value(uint32_t b) {
-  if constexpr (E::kPerVec == 8) return __uint_as_float(b << 16);
-  return __uint_as_float(b);
+  return E::from_bits(b);
 }
 
 template <class E>
@@ -657,25 +689,32 @@ __device__ __forceinline__ void nvls_vecs_f32(char* mc, uint64_t stride_bytes, i
     }
 }
 
-template <int U>
-__device__ __forceinline__ void nvls_vecs_bf16(char* mc, uint64_t stride_bytes, int cnt, float scale) {
+template <class E, int U>
+__device__ __forceinline__ void nvls_vecs_16(char* mc, uint64_t stride_bytes, int cnt, float scale) {
   uint4 v[U];
 #pragma unroll
   for (int u = 0; u < U; ++u)
-    if (u < cnt)
-      asm volatile("multimem.ld_reduce.weak.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
-                   : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
-                   : "l"(mc + u * stride_bytes)
-                   : "memory");
+    if (u < cnt) {
+      if constexpr (std::is_same<E, BF16>::value)
+        asm volatile("multimem.ld_reduce.weak.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                     : "l"(mc + u * stride_bytes)
+                     : "memory");
+      else
+        asm volatile("multimem.ld_reduce.weak.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                     : "l"(mc + u * stride_bytes)
+                     : "memory");
+    }
 #pragma unroll
   for (int u = 0; u < U; ++u)
     if (u < cnt) {
       if (scale != 1.0f) {
         float f[8];
-        BF16::widen(v[u], f);
+        E::widen(v[u], f);
 #pragma unroll
         for (int k = 0; k < 8; ++k) f[k] = __fmul_rn(f[k], scale);
-        v[u] = BF16::narrow(f);
+        v[u] = E::narrow(f);
       }
       asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc + u * stride_bytes),
                    "f"(__uint_as_float(v[u].x)), "f"(__uint_as_float(v[u].y)), "f"(__uint_as_float(v[u].z)),
@@ -702,7 +741,7 @@ __global__ void __launch_bounds__(512) hfr_nvls_kernel(const Args a) {
     for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += U * stride) {
       const int cnt = (int)((hi - i + stride - 1) / stride);
       if constexpr (K == 8)
-        nvls_vecs_bf16<U>(a.mcbuf + i * 16, stride * 16, cnt, a.scale);
+        nvls_vecs_16<E, U>(a.mcbuf + i * 16, stride * 16, cnt, a.scale);
       else
         nvls_vecs_f32<U>(a.mcbuf + i * 16, stride * 16, cnt, a.scale);
     }
@@ -854,13 +893,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
         for (int u = 0; u < 4; ++u) {
           const uint64_t q = q0 + (uint64_t)u * blockDim.x;
           if (q < nq) {
-            if constexpr (E::kPerVec == 8) {
-              const uint2 h = *reinterpret_cast<const uint2*>(mybuf + (base + e0 + q * 4) * 2);
-              f[u][0] = __uint_as_float(h.x << 16); f[u][1] = __uint_as_float(h.x & 0xFFFF0000u);
-              f[u][2] = __uint_as_float(h.y << 16); f[u][3] = __uint_as_float(h.y & 0xFFFF0000u);
-            } else {
-              F32::widen(ld128(mybuf + (base + e0 + q * 4) * 4), f[u]);
-            }
+            F32::widen(ld128(mybuf + (base + e0 + q * 4) * 4), f[u]);  // fp32 only (16-bit: raw copy above)
           }
         }
 #pragma unroll

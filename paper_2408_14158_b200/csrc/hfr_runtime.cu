@@ -200,7 +200,11 @@ uint64_t fnv(uint64_t h, uint64_t v) {
   return h;
 }
 
-size_t dtype_size(hfr_dtype_t t) { return t == HFR_BFLOAT16 ? 2 : 4; }
+size_t dtype_size(hfr_dtype_t t) { return t == HFR_FLOAT32 ? 4 : 2; }
+
+// Kernel instantiation by element type: HFR_BY_DTYPE(dt, M) expands M(F32),
+// M(BF16) or M(F16).
+#define HFR_BY_DTYPE(dt, M) ((dt) == HFR_BFLOAT16 ? (M(BF16)) : (dt) == HFR_FLOAT16 ? (M(F16)) : (M(F32)))
 
 // An explicit ONESHOT on a message above oneshot_max_bytes runs FLAT (same
 // result bits).
@@ -545,9 +549,10 @@ void coll_routing(const hfr_comm_s* c, int coll, int root, int* src, uint32_t* d
 
 hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                       cudaStream_t s, int coll = HFR_ALLREDUCE, int root = 0) {
-  const void* fn = dt == HFR_BFLOAT16 ? flat_fn<BF16>(c->n) : flat_fn<F32>(c->n);
+#define HFR_FLAT_FN(E) flat_fn<E>(c->n)
+  const void* fn = HFR_BY_DTYPE(dt, HFR_FLAT_FN);
   const int threads = cta_threads(c, 512);
-  const uint64_t per = dt == HFR_BFLOAT16 ? 8 : 4;
+  const uint64_t per = dt == HFR_FLOAT32 ? 4 : 8;
   const uint64_t vec_per_rank = count / per / c->n + 1;
   int g = 0;
   HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>((vec_per_rank + threads - 1) / threads, kMaxCtas), &g));
@@ -560,7 +565,8 @@ hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
 
 hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, bool pair, uint64_t sig,
                       cudaStream_t s) {
-  const void* fn = dt == HFR_BFLOAT16 ? tree_fn<BF16>(pair) : tree_fn<F32>(pair);
+#define HFR_TREE_FN(E) tree_fn<E>(pair)
+  const void* fn = HFR_BY_DTYPE(dt, HFR_TREE_FN);
   // 2 CTAs x 256 threads per SM: while one CTA drains its chunk's stores at
   // the per-chunk system fence the other issues (r01: DBT n=4 377 -> 422 GB/s)
   const int threads = cta_threads(c, 256);
@@ -610,13 +616,16 @@ constexpr uint64_t kLLMaxBytes = 64u << 10;  // ONESHOT uses the LL (flag-in-dat
 
 hfr_status_t run_oneshot_ll(hfr_comm_s* c, char* const* local_bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                             cudaStream_t s) {
-  const bool bf = dt == HFR_BFLOAT16;
   const void* fn;
+#define HFR_LL2(E) (const void*)hfr_oneshot_ll_kernel<E, 2>
+#define HFR_LL4(E) (const void*)hfr_oneshot_ll_kernel<E, 4>
+#define HFR_LL8(E) (const void*)hfr_oneshot_ll_kernel<E, 8>
+#define HFR_LL0(E) (const void*)hfr_oneshot_ll_kernel<E, 0>
   switch (c->n) {
-    case 2: fn = bf ? (const void*)hfr_oneshot_ll_kernel<BF16, 2> : (const void*)hfr_oneshot_ll_kernel<F32, 2>; break;
-    case 4: fn = bf ? (const void*)hfr_oneshot_ll_kernel<BF16, 4> : (const void*)hfr_oneshot_ll_kernel<F32, 4>; break;
-    case 8: fn = bf ? (const void*)hfr_oneshot_ll_kernel<BF16, 8> : (const void*)hfr_oneshot_ll_kernel<F32, 8>; break;
-    default: fn = bf ? (const void*)hfr_oneshot_ll_kernel<BF16, 0> : (const void*)hfr_oneshot_ll_kernel<F32, 0>;
+    case 2: fn = HFR_BY_DTYPE(dt, HFR_LL2); break;
+    case 4: fn = HFR_BY_DTYPE(dt, HFR_LL4); break;
+    case 8: fn = HFR_BY_DTYPE(dt, HFR_LL8); break;
+    default: fn = HFR_BY_DTYPE(dt, HFR_LL0);
   }
   const uint64_t npair = (count + 1) / 2;
   // one pair per thread: every word's latency overlaps every other's
@@ -636,8 +645,9 @@ hfr_status_t run_oneshot(hfr_comm_s* c, char* const* local_bufs, uint64_t count,
   // LL form: 8 inbox bytes per element, one NVLink write of latency
   if (count * dtype_size(dt) <= kLLMaxBytes && count * 8 <= c->cfg.oneshot_max_bytes)
     return run_oneshot_ll(c, local_bufs, count, dt, sig, s);
-  const void* fn = dt == HFR_BFLOAT16 ? (const void*)hfr_oneshot_kernel<BF16, 0> : (const void*)hfr_oneshot_kernel<F32, 0>;
-  const uint64_t per = dt == HFR_BFLOAT16 ? 8 : 4;
+#define HFR_ONESHOT_FN(E) (const void*)hfr_oneshot_kernel<E, 0>
+  const void* fn = HFR_BY_DTYPE(dt, HFR_ONESHOT_FN);
+  const uint64_t per = dt == HFR_FLOAT32 ? 4 : 8;
   const uint64_t nvec = count / per;
   // small grids: one CTA per 2048 vectors (32 KiB), at least n threads
   const int min_thr = 32 * ((c->n + 31) / 32);
@@ -747,6 +757,8 @@ hfr_status_t run_ce(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_
                                                                   (f.count / 4 + 511) / 512));
   if (dt == HFR_BFLOAT16)
     hfr_local_fold_kernel<BF16><<<ctas, 512, 0, s>>>(f);
+  else if (dt == HFR_FLOAT16)
+    hfr_local_fold_kernel<F16><<<ctas, 512, 0, s>>>(f);
   else
     hfr_local_fold_kernel<F32><<<ctas, 512, 0, s>>>(f);
   cudaError_t err = cudaGetLastError();
@@ -770,9 +782,10 @@ hfr_status_t run_ce(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_
 
 hfr_status_t run_nvls(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig, uint64_t offset,
                       cudaStream_t s) {
-  const void* fn = dt == HFR_BFLOAT16 ? (const void*)hfr_nvls_kernel<BF16> : (const void*)hfr_nvls_kernel<F32>;
+#define HFR_NVLS_FN(E) (const void*)hfr_nvls_kernel<E>
+  const void* fn = HFR_BY_DTYPE(dt, HFR_NVLS_FN);
   const int threads = cta_threads(c, 512);
-  const uint64_t per = dt == HFR_BFLOAT16 ? 8 : 4;
+  const uint64_t per = dt == HFR_FLOAT32 ? 4 : 8;
   const uint64_t vec_per_rank = count / per / c->n + 1;
   int g = 0;
   HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>((vec_per_rank + threads - 1) / threads, kMaxCtas), &g));
@@ -828,7 +841,7 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
                             cudaStream_t user, hfr_req_t* req, int coll = HFR_ALLREDUCE, int root = 0) {
   if (!c) return HFR_ERR_NOT_INITIALIZED;
   if (req) *req = nullptr;
-  if (dt != HFR_FLOAT32 && dt != HFR_BFLOAT16) return HFR_ERR_INVALID_ARGUMENT;
+  if (dt != HFR_FLOAT32 && dt != HFR_BFLOAT16 && dt != HFR_FLOAT16) return HFR_ERR_INVALID_ARGUMENT;
   if (coll < HFR_ALLREDUCE || coll > HFR_BROADCAST) return HFR_ERR_INVALID_ARGUMENT;
   if ((coll == HFR_REDUCE || coll == HFR_BROADCAST) && (root < 0 || root >= c->n)) return HFR_ERR_INVALID_ARGUMENT;
   if (op != HFR_SUM) return HFR_ERR_UNSUPPORTED;
@@ -1103,9 +1116,9 @@ hfr_status_t hfr_collective_virtual(hfr_comm_t c, hfr_coll_t coll, void* const* 
 
 hfr_status_t hfr_shard_range(int nranks, size_t count, hfr_dtype_t dtype, int rank, size_t* lo, size_t* hi) {
   if (nranks < 1 || nranks > HFR_MAX_RANKS || rank < 0 || rank >= nranks || !lo || !hi ||
-      (dtype != HFR_FLOAT32 && dtype != HFR_BFLOAT16))
+      (dtype != HFR_FLOAT32 && dtype != HFR_BFLOAT16 && dtype != HFR_FLOAT16))
     return HFR_ERR_INVALID_ARGUMENT;
-  const uint64_t K = dtype == HFR_BFLOAT16 ? 8 : 4;  // elements per 16-byte vector
+  const uint64_t K = dtype == HFR_FLOAT32 ? 4 : 8;  // elements per 16-byte vector
   const uint64_t nvec = count / K;
   *lo = K * (nvec * (uint64_t)rank / nranks);
   *hi = rank == nranks - 1 ? count : K * (nvec * (uint64_t)(rank + 1) / nranks);

@@ -15,7 +15,7 @@ def to_torch(x: np.ndarray, device):
 
 def torch_dtype(dtype: str):
     import torch
-    return torch.bfloat16 if dtype == gen.BF16 else torch.float32
+    return {gen.BF16: torch.bfloat16, gen.FP16: torch.float16}.get(dtype, torch.float32)
 
 
 def to_numpy(t) -> np.ndarray:
@@ -28,7 +28,13 @@ def to_numpy(t) -> np.ndarray:
 def as_f32(x: np.ndarray) -> np.ndarray:
     if x.dtype == np.uint16:
         return (x.astype(np.uint32) << np.uint32(16)).view(np.float32)
+    if x.dtype == np.float16:
+        return x.astype(np.float32)
     return x
+
+
+def _bits(x: np.ndarray) -> np.ndarray:
+    return x.view(np.uint16 if x.dtype.itemsize == 2 else np.uint32)
 
 
 def assert_bit_exact(got: np.ndarray, want: np.ndarray, what: str = ""):
@@ -41,8 +47,8 @@ def assert_bit_exact(got: np.ndarray, want: np.ndarray, what: str = ""):
         i = int(np.flatnonzero(gn != wn)[0])
         raise AssertionError(f"{what}: NaN mismatch at {i}: got {g[i]!r} want {w[i]!r}")
     m = ~wn
-    gb = got[m].view(np.uint16 if got.dtype == np.uint16 else np.uint32)
-    wb = want[m].view(np.uint16 if want.dtype == np.uint16 else np.uint32)
+    gb = _bits(got[m])
+    wb = _bits(want[m])
     if not np.array_equal(gb, wb):
         bad = np.flatnonzero(gb != wb)
         idx = np.flatnonzero(m)[bad[:5]]
@@ -65,9 +71,10 @@ def assert_within_r18(got: np.ndarray, xs, want: np.ndarray, scale: float, what:
     assert np.array_equal(np.isnan(g), np.isnan(w)), f"{what}: NaN positions"
     assert np.array_equal(g[~fin], w[~fin]) or not (~fin).any(), f"{what}: Inf mismatch"
     d = np.abs(g[fin] - w[fin])
-    if got.dtype == np.uint16:
-        ex = np.floor(np.log2(np.maximum(np.abs(w[fin]), 2.0 ** -126)))
-        ulp = 2.0 ** (ex - 7)
+    if got.dtype.itemsize == 2:
+        bits, emin = (7, -126) if got.dtype == np.uint16 else (10, -14)
+        ex = np.floor(np.log2(np.maximum(np.abs(w[fin]), 2.0 ** emin)))
+        ulp = 2.0 ** (ex - bits)
         lim = np.maximum(ulp, 8.3e-7 * A[fin] + 0.5 * ulp)
     else:
         lim = 1e-6 * A[fin]

@@ -39,7 +39,7 @@ def gpu_cases(rank, world, port, outdir):
     res = {"rank": rank, "ok": [], "fail": []}
     try:
         comm = hfr.Comm.init(device=rank, config=hfr.Config(timeout_ms=8000, chunk_elems=512))
-        for dtype in (gen.FP32, gen.BF16):
+        for dtype in (gen.FP32, gen.BF16, gen.FP16):
             for algo in ("flat", "oneshot", "dbt", "pair_dbt", "auto", "ce"):
                 if algo == "pair_dbt" and world % 2:
                     continue
@@ -123,7 +123,7 @@ def gpu_cases(rank, world, port, outdir):
         # NVLS order-relaxed path (reading R18 bound), if the box has multicast
         comm = hfr.Comm.init(device=rank, config=hfr.Config(timeout_ms=8000, nvls_bytes=64 << 20, algo="nvls",
                                                             scale=0.5))
-        for dtype in (gen.FP32, gen.BF16):
+        for dtype in (gen.FP32, gen.BF16, gen.FP16):
             for N in (4096 + 13, 1_000_003):
                 for dist_name in ("normal", "int"):
                     xs = gen.rank_inputs(world, N, dtype, dist_name, seed_base=5000 + N)

@@ -40,7 +40,7 @@ def comm_for(hfr, n):
 def run(hfr, n, xs, algo, chunk=512, scale=1.0, symmetric=True, offset=0, async_op=False):
     comm = comm_for(hfr, n)
     comm.set_config(hfr.Config(algo=algo, chunk_elems=chunk, scale=scale))
-    dt = torch_dtype(gen.BF16 if xs[0].dtype == np.uint16 else gen.FP32)
+    dt = torch_dtype({np.dtype(np.uint16): gen.BF16, np.dtype(np.float16): gen.FP16}.get(xs[0].dtype, gen.FP32))
     N = xs[0].shape[0]
     if symmetric:
         bufs = [b[offset:offset + N] for b in comm.empty(N + offset, dt)]
@@ -65,7 +65,7 @@ ALGOS = ["flat", "oneshot", "dbt", "pair_dbt"]
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8])
-@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16])
+@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16, gen.FP16])
 @pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("N", [1, 7, 4096, 4096 + 13, 100_003])
 def test_parity_sizes(hfr, n, dtype, algo, N):
@@ -77,7 +77,7 @@ def test_parity_sizes(hfr, n, dtype, algo, N):
 
 
 @pytest.mark.parametrize("dist", ["specials", "int", "loguniform", "grad"])
-@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16])
+@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16, gen.FP16])
 @pytest.mark.parametrize("algo", ALGOS)
 def test_parity_distributions(hfr, dist, dtype, algo):
     n, N = 8, 3 * 4096 + 5
@@ -199,7 +199,7 @@ def test_cuda_graph_replay(hfr, algo, N):
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
-@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16])
+@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16, gen.FP16])
 @pytest.mark.parametrize("kind", ["reduce_scatter", "allgather", "reduce", "broadcast", "allreduce"])
 @pytest.mark.parametrize("N", [5, 4096 + 13, 300_007])
 def test_collectives(hfr, n, dtype, kind, N):

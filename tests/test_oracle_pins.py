@@ -457,3 +457,59 @@ def test_tree_n1_degenerate():
     assert pa == [-1] and pb == [-1] and ca == [[]] and cb == [[]]
     with pytest.raises(ValueError):
         O.build_double_binary_tree(0)
+
+
+# ----------------------------------------------------------------------------
+# fp16 (PAPER.md:404 lists FP16): fp32 accumulate, one RNE rounding to binary16
+# ----------------------------------------------------------------------------
+
+def f16_round(q: Fraction):
+    return _round_binary(q, 11, -14, 15)
+
+
+def exact_f16(y: float) -> float:
+    if math.isnan(y) or math.isinf(y) or y == 0:
+        return y
+    return float(f16_round(Fraction(y)))
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("dist", ["normal", "loguniform", "specials"])
+def test_fold_ascending_fp16_brute_force(n, dist):
+    xs = gen.rank_inputs(n, 64, gen.FP16, dist, seed_base=199 + n)
+    scale = 0.5 if n > 2 else 1.0
+    got = O.fold_ascending(xs, scale=scale).astype(np.float32)
+    cols = list(zip(*[x.astype(np.float32).tolist() for x in xs]))
+    want = []
+    for vals in cols:
+        acc = float(vals[0])
+        for v in vals[1:]:
+            acc = exact_add(acc, float(v))
+        want.append(exact_f16(exact_mul(acc, scale)))
+    assert _same_f32(got, want)
+
+
+def test_fp16_rne_matches_torch_and_hand_cases():
+    import torch
+    rng = np.random.default_rng(1)
+    f = rng.integers(0, 2 ** 32, size=1 << 20, dtype=np.uint64).astype(np.uint32).view(np.float32)
+    got = O._finish(f, 1.0, O.F16)
+    want = torch.tensor(f).to(torch.float16).numpy()
+    nan = np.isnan(f)
+    assert np.array_equal(got[~nan].view(np.uint16), want[~nan].view(np.uint16))
+    assert np.all(np.isnan(got[nan]))
+    # hand cases: 2049 ties to 2048, 2051 ties to 2052, 65520 overflows to inf, 2^-25 ties to 0
+    cases = [(2049.0, 2048.0), (2051.0, 2052.0), (65519.0, 65504.0), (65520.0, np.inf), (2.0 ** -25, 0.0),
+             (3 * 2.0 ** -25, 2.0 ** -23)]
+    for v, w in cases:
+        assert float(O._finish(np.array([v], np.float32), 1.0, O.F16)[0]) == w, v
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("algo", ["flat", "dbt", "pair_dbt"])
+def test_integer_closed_form_fp16(n, algo):
+    """|x| <= 256, n <= 8: sums <= 2048 are exact in fp32 and in binary16."""
+    xs = gen.rank_inputs(n, 2000, gen.FP16, "int", seed_base=13)
+    want = sum(x.astype(np.int64) for x in xs)
+    got = O.allreduce(xs, algo, chunk_elems=256)[0]
+    assert np.array_equal(got.astype(np.int64), want)
