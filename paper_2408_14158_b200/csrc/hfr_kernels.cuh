@@ -874,8 +874,11 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
       for (int sl = 0; sl < nchild; ++sl) slot_bf16[sl] = a.tree[c & 1][nd.child[sl]].nchild == 0;
     }
     if (leafcopy && E::kPerVec == 8) {
+      // raw 16-bit partials live in the first half of the chunk's fp32 slot
+      // region (bytes [4*e0, 4*e0 + 2*C)), so they never overlap another
+      // chunk's fp32 partials in the same slot array
       const char* srcb = mybuf + (base + e0) * 2;
-      char* dstb = reinterpret_cast<char*>(dst_part) + e0 * 2;
+      char* dstb = reinterpret_cast<char*>(dst_part + e0);
       for (uint64_t q0 = threadIdx.x; q0 < nv; q0 += (uint64_t)blockDim.x * 4) {
         uint4 v[4];
 #pragma unroll
@@ -924,7 +927,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
         for (int sl = 0; sl < 2; ++sl)
           if (sl < nchild) {
             if (E::kPerVec == 8 && slot_bf16[sl])
-              load8<E>(reinterpret_cast<const char*>(mypart + (uint64_t)sl * a.part_stride), e, pp[u][sl]);
+              load8<E>(reinterpret_cast<const char*>(mypart + (uint64_t)sl * a.part_stride + e0), e - e0, pp[u][sl]);
             else
               load8_f32(mypart + (uint64_t)sl * a.part_stride, e, pp[u][sl]);
           }
@@ -970,7 +973,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
         if (k != nd.self_pos) {
           const int sl = k < nd.self_pos ? k : k - 1;
           const float* slot = mypart + (uint64_t)sl * a.part_stride;
-          s = (E::kPerVec == 8 && slot_bf16[sl]) ? E::load1(reinterpret_cast<const char*>(slot), e) : slot[e];
+          s = (E::kPerVec == 8 && slot_bf16[sl]) ? E::load1(reinterpret_cast<const char*>(slot + e0), e - e0) : slot[e];
         }
         acc = k == 0 ? s : __fadd_rn(acc, s);
       }
@@ -980,7 +983,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
         for (int k = 0; k < nd.nchild; ++k) E::store1(a.buf[member(nd.child[k])], base + e, acc);
         if constexpr (PAIR) E::store1(pbuf, base + e, acc);
       } else if (E::kPerVec == 8 && leafcopy) {
-        E::store1(reinterpret_cast<char*>(dst_part), e, acc);  // raw bf16 leaf partial (exact)
+        E::store1(reinterpret_cast<char*>(dst_part + e0), e - e0, acc);  // raw 16-bit leaf partial (exact)
       } else {
         dst_part[e] = acc;
       }
