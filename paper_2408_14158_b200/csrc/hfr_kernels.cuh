@@ -246,6 +246,38 @@ __device__ __forceinline__ void exit_barrier(const Args& a, int rank, int b, uin
   __syncthreads();
 }
 
+// Exit through the NVLS multicast arena: after its stores (incl. multimem.st)
+// each CTA b bumps counter b on every GPU with ONE multimem.red.release and
+// waits until all n ranks' CTA b arrived (k = this CTA's NVLS launch count).
+__device__ __forceinline__ void mc_exit_barrier(const Args& a, int b, int n, uint32_t k) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t target = (uint32_t)n * k;
+    asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(a.mc_exit + b) : "memory");
+    uint64_t t_start = 0;
+    for (uint32_t it = 1;; ++it) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.uc_exit + b) : "memory");
+      if ((int32_t)(v - target) >= 0) break;
+      if ((it & 1023u) == 0) {
+        if (!t_start) t_start = globaltimer();
+        if (*a.err != 0) break;
+        if (globaltimer() - t_start > a.timeout_ns) {
+          raise_error(a, kErrTimeout);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void mc_st128(char* mc, const uint4& v) {
+  asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(mc), "f"(__uint_as_float(v.x)),
+               "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
+               : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // element types
 // ---------------------------------------------------------------------------
@@ -337,7 +369,7 @@ struct F16 {
 // ---------------------------------------------------------------------------
 template <class E, int NR, int U>
 __device__ __forceinline__ void flat_vecs(const Args& a, uint64_t i, uint64_t stride, uint64_t hi, int src,
-                                          uint32_t dmask) {
+                                          uint32_t dmask, char* mc) {
   // U vectors per thread, all loads issued before the first fold so that
   // U*NR 16-byte NVLink reads are in flight per thread.  src >= 0: copy that
   // rank's vectors (all-gather / broadcast) instead of folding all ranks.
@@ -381,9 +413,13 @@ __device__ __forceinline__ void flat_vecs(const Args& a, uint64_t i, uint64_t st
 #pragma unroll
       for (int k = 0; k < K; ++k) acc[k] = __fmul_rn(acc[k], a.scale);
       const uint4 o = E::narrow(acc);
+      if (mc) {
+        mc_st128(mc + (i + u * stride) * 16, o);  // NVSwitch multicast: one store reaches all n buffers
+      } else {
 #pragma unroll
-      for (int r = 0; r < NR; ++r)
-        if ((dmask >> r) & 1u) st128(a.buf[r] + (i + u * stride) * 16, o);
+        for (int r = 0; r < NR; ++r)
+          if ((dmask >> r) & 1u) st128(a.buf[r] + (i + u * stride) * 16, o);
+      }
     }
   }
 }
@@ -424,6 +460,11 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
   // -> all; broadcast = root's shard -> all
   const int src = a.src_rank == -2 ? rank : a.src_rank;
   const uint32_t dmask = a.dst_mask ? a.dst_mask : (1u << rank);
+  // FLAT over an NVLS arena (allreduce only): the owner's result goes out as
+  // one multimem.st (the all-gather half), exit via the multicast counters.
+  // Bits are unchanged: the fold is still this CTA's, in rank order.
+  __shared__ uint32_t s_k;
+  if (a.mcbuf && threadIdx.x == 0) s_k = ++a.pad[rank]->nvls_seq[b];
   // shard owners: all n ranks, or (reduce / broadcast) the n-1 ranks other
   // than the root, so the root's link carries each byte once
   const int nown = a.excl_root >= 0 ? n - 1 : n;
@@ -443,7 +484,7 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
       const uint64_t warps = stride / 32;
       const uint64_t w = ((uint64_t)b * blockDim.x + threadIdx.x) / 32;
       for (uint64_t t0 = lo + w * (U * 32); t0 < hi; t0 += warps * (U * 32))
-        flat_vecs<E, NR, U>(a, t0 + lane, 32, hi, src, dmask);
+        flat_vecs<E, NR, U>(a, t0 + lane, 32, hi, src, dmask, a.mcbuf);
     } else {
       for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += stride)
         flat_vec_dyn<E>(a, n, i, src, dmask);
@@ -472,7 +513,10 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
       }
     }
   }
-  exit_barrier(a, rank, b, e);
+  if (a.mcbuf)
+    mc_exit_barrier(a, b, n, s_k);
+  else
+    exit_barrier(a, rank, b, e);
   end_epoch(a.pad[rank], e);
 }
 
@@ -754,26 +798,7 @@ __global__ void __launch_bounds__(512) hfr_nvls_kernel(const Args a) {
       acc = __fmul_rn(acc, a.scale);
       for (int r = 0; r < n; ++r) E::store1(a.buf[r], el, acc);
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const uint32_t target = (uint32_t)n * s_k;
-      asm volatile("multimem.red.release.sys.global.add.u32 [%0], 1;" ::"l"(a.mc_exit + b) : "memory");
-      uint64_t t_start = 0;
-      for (uint32_t it = 1;; ++it) {
-        uint32_t v;
-        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.uc_exit + b) : "memory");
-        if ((int32_t)(v - target) >= 0) break;
-        if ((it & 1023u) == 0) {
-          if (!t_start) t_start = globaltimer();
-          if (*a.err != 0) break;
-          if (globaltimer() - t_start > a.timeout_ns) {
-            raise_error(a, kErrTimeout);
-            break;
-          }
-        }
-      }
-    }
-    __syncthreads();
+    mc_exit_barrier(a, b, n, s_k);
   }
   end_epoch(mine, e);
 }

@@ -548,7 +548,8 @@ void coll_routing(const hfr_comm_s* c, int coll, int root, int* src, uint32_t* d
 }
 
 hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
-                      cudaStream_t s, int coll = HFR_ALLREDUCE, int root = 0) {
+                      cudaStream_t s, int coll = HFR_ALLREDUCE, int root = 0, const Region* reg = nullptr,
+                      uint64_t offset = 0) {
 #define HFR_FLAT_FN(E) flat_fn<E>(c->n)
   const void* fn = HFR_BY_DTYPE(dt, HFR_FLAT_FN);
   const int threads = cta_threads(c, 512);
@@ -560,6 +561,16 @@ hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   base_args(c, a, count, fnv(sig, (uint64_t)g * 1315423911ull + threads));
   for (int q = 0; q < c->n; ++q) a.buf[q] = bufs[q];
   coll_routing(c, coll, root, &a.src_rank, &a.dst_mask, &a.excl_root);
+  // buffer inside the NVLS arena: multicast all-gather half (same bits);
+  // HFR_FLAT_MC=0 turns it off (A/B experiments)
+  static const bool mc_ok = !getenv("HFR_FLAT_MC") || strcmp(getenv("HFR_FLAT_MC"), "0") != 0;
+  if (mc_ok && coll == HFR_ALLREDUCE && reg && reg->nvls && c->nvls && c->nvls->on) {
+    a.mcbuf = (char*)c->nvls->mcva + offset;
+    a.mc_exit = (uint32_t*)c->nvls->mcva;
+    a.uc_exit = (uint32_t*)c->nvls->uc[c->rank];
+    sig = fnv(sig, 0x4d43);
+    a.sig = fnv(sig, (uint64_t)g * 1315423911ull + threads);
+  }
   return launch(c, fn, g, threads, a, s);
 }
 
@@ -920,7 +931,7 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     } else if (algo == HFR_ALGO_CE && zero_copy) {
       HFR_TRY(run_ce(c, bufs, count, dt, s));
     } else if (algo == HFR_ALGO_FLAT || algo == HFR_ALGO_CE) {
-      HFR_TRY(run_flat(c, bufs, count, dt, sig, s, coll, root));
+      HFR_TRY(run_flat(c, bufs, count, dt, sig, s, coll, root, zero_copy ? reg : nullptr, offset));
     } else {
       HFR_TRY(run_tree(c, bufs, count, dt, algo == HFR_ALGO_PAIR_DBT, sig, s));
     }
