@@ -41,6 +41,7 @@ struct Pad {
   uint64_t ce_done[kMaxRanks];  //   rank q's result shard is final
   uint64_t ce_exit[kMaxRanks];  //   rank q finished pulling from every peer
   uint32_t nvls_seq[kMaxCtas]; // NVLS launches seen by CTA b (local only)
+  uint64_t tile_next;           // FLAT: next warp tile to hand out (dynamic distribution), 0 between launches
   uint64_t launch_epoch;        // epoch of the last completed launch on this rank
   uint32_t done_ctas;           // CTAs of the current launch that have finished
 };
@@ -78,6 +79,7 @@ struct Args {
   int ntree;               // nodes per tree (n, or n/2 for PAIR)
   int src_rank;            // FLAT kernel: -1 fold all ranks; -2 copy my own shard; r>=0 copy rank r's
   uint32_t dst_mask;       // FLAT kernel: ranks that receive the result (0 = the owner itself)
+  int dyn_tiles;           // FLAT kernel: warps grab tiles from a per-rank counter (no tail imbalance)
   int excl_root;           // FLAT kernel: >= 0: this rank owns no shard (reduce/broadcast root)
   char* mcbuf;              // NVLS: multicast VA of this call's buffer
   uint32_t* mc_exit;       // NVLS: multicast VA of the exit counters [kMaxCtas]
@@ -154,6 +156,7 @@ __device__ __forceinline__ void end_epoch(Pad* mine, uint64_t e) {
     __threadfence();
     if (atomicAdd(&mine->done_ctas, 1u) == gridDim.x - 1) {
       mine->done_ctas = 0;
+      mine->tile_next = 0;  // every CTA of this launch is past its last tile grab
       *reinterpret_cast<volatile uint64_t*>(&mine->launch_epoch) = e;
       __threadfence();
     }
@@ -481,10 +484,24 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
       // buffer): lane l of the warp owning tile t handles vectors
       // t*U*32 + u*32 + l, u < U.  Tiles are dealt round-robin to all warps.
       const uint64_t lane = threadIdx.x & 31;
-      const uint64_t warps = stride / 32;
-      const uint64_t w = ((uint64_t)b * blockDim.x + threadIdx.x) / 32;
-      for (uint64_t t0 = lo + w * (U * 32); t0 < hi; t0 += warps * (U * 32))
-        flat_vecs<E, NR, U>(a, t0 + lane, 32, hi, src, dmask, a.mcbuf);
+      if (a.dyn_tiles) {
+        // dynamic: each warp takes the next tile of this rank's shard from a
+        // counter in the local pad, so fast CTAs absorb the slow ones' share
+        unsigned long long* ctr = reinterpret_cast<unsigned long long*>(&a.pad[rank]->tile_next);
+        for (;;) {
+          uint64_t t = 0;
+          if (lane == 0) t = atomicAdd(ctr, 1ull);
+          t = __shfl_sync(0xffffffffu, t, 0);
+          const uint64_t t0 = lo + t * (U * 32);
+          if (t0 >= hi) break;
+          flat_vecs<E, NR, U>(a, t0 + lane, 32, hi, src, dmask, a.mcbuf);
+        }
+      } else {
+        const uint64_t warps = stride / 32;
+        const uint64_t w = ((uint64_t)b * blockDim.x + threadIdx.x) / 32;
+        for (uint64_t t0 = lo + w * (U * 32); t0 < hi; t0 += warps * (U * 32))
+          flat_vecs<E, NR, U>(a, t0 + lane, 32, hi, src, dmask, a.mcbuf);
+      }
     } else {
       for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += stride)
         flat_vec_dyn<E>(a, n, i, src, dmask);

@@ -561,6 +561,8 @@ hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   base_args(c, a, count, fnv(sig, (uint64_t)g * 1315423911ull + threads));
   for (int q = 0; q < c->n; ++q) a.buf[q] = bufs[q];
   coll_routing(c, coll, root, &a.src_rank, &a.dst_mask, &a.excl_root);
+  static const bool dyn = !getenv("HFR_DYN_TILES") || strcmp(getenv("HFR_DYN_TILES"), "0") != 0;
+  a.dyn_tiles = dyn ? 1 : 0;
   // buffer inside the NVLS arena: multicast all-gather half (same bits).
   // Opt-in (HFR_FLAT_MC=1): measured slower on 2/4 B200s (r01: n=4 bf16 1 GiB
   // 579 vs 659 GB/s with unicast stores), kept for n=8 experiments.
