@@ -799,12 +799,21 @@ __global__ void __launch_bounds__(512) hfr_nvls_kernel(const Args a) {
     const uint64_t lo = nvec * rank / n, hi = nvec * (rank + 1) / n;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     constexpr int U = 4;
-    for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += U * stride) {
-      const int cnt = (int)((hi - i + stride - 1) / stride);
+    (void)stride;
+    // warp tiles of U*32 vectors handed out from the per-rank counter (as FLAT)
+    const uint64_t lane = threadIdx.x & 31;
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(&mine->tile_next);
+    for (;;) {
+      uint64_t t = 0;
+      if (lane == 0) t = atomicAdd(ctr, 1ull);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      const uint64_t i = lo + t * (U * 32) + lane;
+      if (lo + t * (U * 32) >= hi) break;
+      const int cnt = i < hi ? (int)((hi - i + 31) / 32) : 0;
       if constexpr (K == 8)
-        nvls_vecs_16<E, U>(a.mcbuf + i * 16, stride * 16, cnt, a.scale);
+        nvls_vecs_16<E, U>(a.mcbuf + i * 16, 32 * 16, cnt < U ? cnt : U, a.scale);
       else
-        nvls_vecs_f32<U>(a.mcbuf + i * 16, stride * 16, cnt, a.scale);
+        nvls_vecs_f32<U>(a.mcbuf + i * 16, 32 * 16, cnt < U ? cnt : U, a.scale);
     }
     // ragged tail (< K elements): the last rank folds it over unicast peers
     const uint64_t t0 = nvec * K;
