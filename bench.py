@@ -380,16 +380,19 @@ def main():
             try:
                 for _ in range(2):
                     step()
-            except hfr.HfrError as e:
-                variants[algo] = {"unavailable": nvls_note or str(e)}
+                tv, _ = timed(step, max(3, args.steps // 2))
+            except hfr.HfrError as e:  # context only: never lose the headline line over a variant
+                variants[algo] = {"unavailable": (nvls_note if algo == "nvls" and nvls_note else str(e))}
+                if comm.status() != hfr.SUCCESS:
+                    break
                 continue
-            tv, _ = timed(step, max(3, args.steps // 2))
             variants[algo] = {"busbw": busbw(S, tv, n), "ms_per_step": tv * 1e3}
             if algo == "nvls":
                 variants[algo]["numerics"] = "order-relaxed (NVSwitch reduction), held to DESIGN.md R18, not bit-exact"
             else:
                 variants[algo]["numerics"] = "bit-exact vs the tree-order / pair-first oracle"
-        comm.set_config(cfg)
+        if comm.status() == hfr.SUCCESS:
+            comm.set_config(cfg)
 
     cpu = None
     if rank == 0 and not multi and not args.no_cpu:
