@@ -538,6 +538,123 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
 }
 
 // ---------------------------------------------------------------------------
+// FLAT with TMA staging (north star: "shared-memory or TMA double-buffered
+// staging"): per CTA, one elected thread moves tile t of shard g from all n
+// ranks' buffers into shared memory with cp.async.bulk (the TMA bulk-copy
+// engine, completion counted on an mbarrier), two stages deep; the CTA folds
+// stage s from shared memory in rank order while stage s^1 is in flight, then
+// stores the result to every rank from registers.  Same arithmetic, same bits
+// as hfr_flat_kernel; tiles come from the per-rank counter.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n HFR_MBAR_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra HFR_MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int kTmaTileBytes = 4096;  // per source per stage
+
+template <class E, int NR>
+__global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
+  extern __shared__ __align__(128) uint8_t stage_mem[];  // [2][NR][kTmaTileBytes]
+  __shared__ uint64_t bars[2];
+  __shared__ uint64_t s_tile[2];
+  const int rank = a.rank0 + blockIdx.y;
+  const int b = blockIdx.x;
+  const uint64_t e = begin_epoch(a.pad[rank]);
+  const uint32_t dmask = a.dst_mask ? a.dst_mask : (1u << rank);
+  if (entry_barrier(a, rank, b, e)) {
+    constexpr int K = E::kPerVec;
+    constexpr uint64_t TV = kTmaTileBytes / 16;  // vectors per tile
+    const uint64_t nvec = a.count / K;
+    const uint64_t lo = nvec * rank / NR, hi = nvec * (rank + 1) / NR;
+    const uint64_t ntile = (hi - lo + TV - 1) / TV;
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(&a.pad[rank]->tile_next);
+    auto issue = [&](int st, uint64_t t) {  // thread 0 only
+      const uint64_t v0 = lo + t * TV;
+      const uint32_t bytes = (uint32_t)((v0 + TV < hi ? TV : hi - v0) * 16);
+      mbar_expect_tx(&bars[st], NR * bytes);
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        bulk_g2s(stage_mem + ((size_t)st * NR + r) * kTmaTileBytes, a.buf[r] + v0 * 16, bytes, &bars[st]);
+    };
+    if (threadIdx.x == 0) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+      for (int st = 0; st < 2; ++st) {
+        const uint64_t t = atomicAdd(ctr, 1ull);
+        s_tile[st] = t;
+        if (t < ntile) issue(st, t);
+      }
+    }
+    __syncthreads();
+    for (uint32_t k = 0;; ++k) {
+      const int st = k & 1;
+      const uint64_t t = s_tile[st];
+      if (t >= ntile) break;
+      mbar_wait(&bars[st], (k >> 1) & 1);
+      const uint64_t v0 = lo + t * TV;
+      const uint64_t nv = v0 + TV < hi ? TV : hi - v0;
+      const uint8_t* sm = stage_mem + (size_t)st * NR * kTmaTileBytes;
+      for (uint64_t j = threadIdx.x; j < nv; j += blockDim.x) {
+        float acc[K], tt[K];
+        E::widen(*reinterpret_cast<const uint4*>(sm + j * 16), acc);
+#pragma unroll
+        for (int r = 1; r < NR; ++r) {
+          E::widen(*reinterpret_cast<const uint4*>(sm + (size_t)r * kTmaTileBytes + j * 16), tt);
+#pragma unroll
+          for (int q = 0; q < K; ++q) acc[q] = __fadd_rn(acc[q], tt[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < K; ++q) acc[q] = __fmul_rn(acc[q], a.scale);
+        const uint4 o = E::narrow(acc);
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+          if ((dmask >> r) & 1u) st128(a.buf[r] + (v0 + j) * 16, o);
+      }
+      __syncthreads();  // every thread is done reading stage st
+      if (threadIdx.x == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async-proxy refill
+        const uint64_t tn = atomicAdd(ctr, 1ull);
+        s_tile[st] = tn;
+        if (tn < ntile) issue(st, tn);
+      }
+      __syncthreads();
+    }
+    // ragged tail (< K elements) — last rank, CTA 0
+    const uint64_t t0 = nvec * K;
+    if (rank == NR - 1 && b == 0 && threadIdx.x < a.count - t0) {
+      const uint64_t el = t0 + threadIdx.x;
+      float acc = E::load1(a.buf[0], el);
+      for (int r = 1; r < NR; ++r) acc = __fadd_rn(acc, E::load1(a.buf[r], el));
+      acc = __fmul_rn(acc, a.scale);
+      for (int r = 0; r < NR; ++r)
+        if ((dmask >> r) & 1u) E::store1(a.buf[r], el, acc);
+    }
+  }
+  exit_barrier(a, rank, b, e);
+  end_epoch(a.pad[rank], e);
+}
+
+// ---------------------------------------------------------------------------
 // ONESHOT (small messages): push, then fold locally.
 //
 // CTA b of rank r stores its slice of x_r into slot [epoch&1][r] of every

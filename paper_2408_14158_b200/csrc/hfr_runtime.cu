@@ -473,6 +473,16 @@ const void* flat_fn(int n) {
 }
 
 template <class E>
+const void* flat_tma_fn(int n) {
+  switch (n) {
+    case 2: return (const void*)hfr_flat_tma_kernel<E, 2>;
+    case 4: return (const void*)hfr_flat_tma_kernel<E, 4>;
+    case 8: return (const void*)hfr_flat_tma_kernel<E, 8>;
+    default: return nullptr;
+  }
+}
+
+template <class E>
 const void* tree_fn(bool pair) {
   return pair ? (const void*)hfr_tree_kernel<E, true> : (const void*)hfr_tree_kernel<E, false>;
 }
@@ -547,9 +557,52 @@ void coll_routing(const hfr_comm_s* c, int coll, int root, int* src, uint32_t* d
   }
 }
 
+// TMA-staged FLAT (experiment, HFR_FLAT_TMA=1): allreduce / reduce-scatter
+// with n in {2, 4, 8}
+hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
+                          cudaStream_t s, int coll, int root, const void* fn) {
+  const int threads = 256;
+  const int smem = 2 * c->n * kTmaTileBytes;
+  static bool attr_done[3][3] = {};
+  const int di = dt == HFR_FLOAT32 ? 0 : dt == HFR_BFLOAT16 ? 1 : 2, ni = c->n == 2 ? 0 : c->n == 4 ? 1 : 2;
+  if (!attr_done[di][ni]) {
+    HFR_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_done[di][ni] = true;
+  }
+  int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : 2 * c->num_sms;
+  if (c->virt && c->local > 1) {
+    int occ = 0;
+    HFR_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
+    g = std::min(g, occ * c->num_sms / c->local);
+  }
+  g = std::max(1, std::min(g, kMaxCtas));
+  Args a;
+  base_args(c, a, count, fnv(fnv(sig, 0x544d41), (uint64_t)g * 1315423911ull + threads));
+  for (int q = 0; q < c->n; ++q) a.buf[q] = bufs[q];
+  int excl = -1;
+  coll_routing(c, coll, root, &a.src_rank, &a.dst_mask, &excl);
+  ++c->epoch;
+  void* params[] = {&a};
+  cudaError_t e = (c->virt && c->local > 1)
+                      ? cudaLaunchCooperativeKernel(fn, dim3(g, c->local), dim3(threads), params, smem, s)
+                      : cudaLaunchKernel(fn, dim3(g, c->local), dim3(threads), params, smem, s);
+  if (e != cudaSuccess) {
+    note_cuda(e, "hfr_flat_tma_kernel");
+    return HFR_ERR_CUDA;
+  }
+  ++c->launches;
+  return HFR_SUCCESS;
+}
+
 hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                       cudaStream_t s, int coll = HFR_ALLREDUCE, int root = 0, const Region* reg = nullptr,
                       uint64_t offset = 0) {
+  static const bool tma = getenv("HFR_FLAT_TMA") && strcmp(getenv("HFR_FLAT_TMA"), "1") == 0;
+  if (tma && (coll == HFR_ALLREDUCE || coll == HFR_REDUCE_SCATTER)) {
+#define HFR_TMA_FN(E) flat_tma_fn<E>(c->n)
+    const void* tfn = HFR_BY_DTYPE(dt, HFR_TMA_FN);
+    if (tfn) return run_flat_tma(c, bufs, count, dt, sig, s, coll, root, tfn);
+  }
 #define HFR_FLAT_FN(E) flat_fn<E>(c->n)
   const void* fn = HFR_BY_DTYPE(dt, HFR_FLAT_FN);
   const int threads = cta_threads(c, 512);

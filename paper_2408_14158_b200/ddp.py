@@ -66,7 +66,7 @@ class HaiScaleDDP:
     """Gradient arena + asynchronous bucketed allreduce for one rank.
 
     Usage per step:
-        ddp.zero_grad()                     (optional)
+        ddp.zero_grad()                     (optional; the backward may overwrite instead)
         for i in backward order: write ddp.grad(i); ddp.mark_ready(i, stream)
         ddp.finish(stream)                  (stream waits for every bucket)
     """
@@ -89,6 +89,9 @@ class HaiScaleDDP:
                 self._bucket_of_param[i].append(k)
         self._works = []
         self.stats = BucketStats()
+
+    def zero_grad(self):
+        self.arena.zero_()
 
     def grad(self, i: int):
         s, e = self.param_ranges[i]
