@@ -557,8 +557,7 @@ void coll_routing(const hfr_comm_s* c, int coll, int root, int* src, uint32_t* d
   }
 }
 
-// TMA-staged FLAT (experiment, HFR_FLAT_TMA=1): allreduce / reduce-scatter
-// with n in {2, 4, 8}
+// TMA-staged FLAT (default for allreduce / reduce-scatter with n in {2, 4, 8})
 hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                           cudaStream_t s, int coll, int root, const void* fn) {
   const int threads = 256;
@@ -597,7 +596,10 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
 hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                       cudaStream_t s, int coll = HFR_ALLREDUCE, int root = 0, const Region* reg = nullptr,
                       uint64_t offset = 0) {
-  static const bool tma = getenv("HFR_FLAT_TMA") && strcmp(getenv("HFR_FLAT_TMA"), "1") == 0;
+  // TMA-staged variant by default for n in {2,4,8} (r01: +2.5-4 % over the
+  // register-staged kernel; 99.5 % of HBM with 8 virtual ranks); HFR_FLAT_TMA=0
+  // selects the register-staged kernel
+  static const bool tma = !getenv("HFR_FLAT_TMA") || strcmp(getenv("HFR_FLAT_TMA"), "0") != 0;
   if (tma && (coll == HFR_ALLREDUCE || coll == HFR_REDUCE_SCATTER)) {
 #define HFR_TMA_FN(E) flat_tma_fn<E>(c->n)
     const void* tfn = HFR_BY_DTYPE(dt, HFR_TMA_FN);
