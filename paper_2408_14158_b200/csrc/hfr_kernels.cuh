@@ -80,6 +80,7 @@ struct Args {
   int src_rank;            // FLAT kernel: -1 fold all ranks; -2 copy my own shard; r>=0 copy rank r's
   uint32_t dst_mask;       // FLAT kernel: ranks that receive the result (0 = the owner itself)
   int dyn_tiles;           // FLAT kernel: warps grab tiles from a per-rank counter (no tail imbalance)
+  int tma_tile;            // FLAT TMA kernel: bytes per source per stage (multiple of 16)
   int excl_root;           // FLAT kernel: >= 0: this rank owns no shard (reduce/broadcast root)
   char* mcbuf;              // NVLS: multicast VA of this call's buffer
   uint32_t* mc_exit;       // NVLS: multicast VA of the exit counters [kMaxCtas]
@@ -571,11 +572,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-constexpr int kTmaTileBytes = 4096;  // per source per stage
+constexpr int kTmaTileBytes = 4096;  // default bytes per source per stage (a.tma_tile)
 
 template <class E, int NR>
 __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
-  extern __shared__ __align__(128) uint8_t stage_mem[];  // [2][NR][kTmaTileBytes]
+  extern __shared__ __align__(128) uint8_t stage_mem[];  // [2][NR][a.tma_tile]
   __shared__ uint64_t bars[2];
   __shared__ uint64_t s_tile[2];
   const int rank = a.rank0 + blockIdx.y;
@@ -584,7 +585,8 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
   const uint32_t dmask = a.dst_mask ? a.dst_mask : (1u << rank);
   if (entry_barrier(a, rank, b, e)) {
     constexpr int K = E::kPerVec;
-    constexpr uint64_t TV = kTmaTileBytes / 16;  // vectors per tile
+    const uint64_t TB = (uint64_t)a.tma_tile;    // bytes per source per stage
+    const uint64_t TV = TB / 16;                 // vectors per tile
     const uint64_t nvec = a.count / K;
     const uint64_t lo = nvec * rank / NR, hi = nvec * (rank + 1) / NR;
     const uint64_t ntile = (hi - lo + TV - 1) / TV;
@@ -595,7 +597,7 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
       mbar_expect_tx(&bars[st], NR * bytes);
 #pragma unroll
       for (int r = 0; r < NR; ++r)
-        bulk_g2s(stage_mem + ((size_t)st * NR + r) * kTmaTileBytes, a.buf[r] + v0 * 16, bytes, &bars[st]);
+        bulk_g2s(stage_mem + ((size_t)st * NR + r) * TB, a.buf[r] + v0 * 16, bytes, &bars[st]);
     };
     if (threadIdx.x == 0) {
       mbar_init(&bars[0], 1);
@@ -616,13 +618,13 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
       mbar_wait(&bars[st], (k >> 1) & 1);
       const uint64_t v0 = lo + t * TV;
       const uint64_t nv = v0 + TV < hi ? TV : hi - v0;
-      const uint8_t* sm = stage_mem + (size_t)st * NR * kTmaTileBytes;
+      const uint8_t* sm = stage_mem + (size_t)st * NR * TB;
       for (uint64_t j = threadIdx.x; j < nv; j += blockDim.x) {
         float acc[K], tt[K];
         E::widen(*reinterpret_cast<const uint4*>(sm + j * 16), acc);
 #pragma unroll
         for (int r = 1; r < NR; ++r) {
-          E::widen(*reinterpret_cast<const uint4*>(sm + (size_t)r * kTmaTileBytes + j * 16), tt);
+          E::widen(*reinterpret_cast<const uint4*>(sm + (size_t)r * TB + j * 16), tt);
 #pragma unroll
           for (int q = 0; q < K; ++q) acc[q] = __fadd_rn(acc[q], tt[q]);
         }

@@ -560,15 +560,13 @@ void coll_routing(const hfr_comm_s* c, int coll, int root, int* src, uint32_t* d
 // TMA-staged FLAT (default for allreduce / reduce-scatter with n in {2, 4, 8})
 hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                           cudaStream_t s, int coll, int root, const void* fn) {
-  const int threads = 256;
-  const int smem = 2 * c->n * kTmaTileBytes;
-  static bool attr_done[3][3] = {};
-  const int di = dt == HFR_FLOAT32 ? 0 : dt == HFR_BFLOAT16 ? 1 : 2, ni = c->n == 2 ? 0 : c->n == 4 ? 1 : 2;
-  if (!attr_done[di][ni]) {
-    HFR_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_done[di][ni] = true;
-  }
-  int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : 2 * c->num_sms;
+  // experiment knobs: HFR_TMA_TILE (bytes per source per stage), HFR_TMA_PER_SM
+  static const int tile = getenv("HFR_TMA_TILE") ? atoi(getenv("HFR_TMA_TILE")) : kTmaTileBytes;
+  static const int per_sm = getenv("HFR_TMA_PER_SM") ? atoi(getenv("HFR_TMA_PER_SM")) : 2;
+  const int threads = cta_threads(c, 256);
+  const int smem = 2 * c->n * tile;
+  HFR_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : per_sm * c->num_sms;
   if (c->virt && c->local > 1) {
     int occ = 0;
     HFR_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
@@ -578,6 +576,7 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
   Args a;
   base_args(c, a, count, fnv(fnv(sig, 0x544d41), (uint64_t)g * 1315423911ull + threads));
   for (int q = 0; q < c->n; ++q) a.buf[q] = bufs[q];
+  a.tma_tile = tile;
   int excl = -1;
   coll_routing(c, coll, root, &a.src_rank, &a.dst_mask, &excl);
   ++c->epoch;
