@@ -301,11 +301,14 @@ def main():
 
     value = busbw(S, t_step, n)
     hbm_peak, hbm_src = peaks()
+    # the step's one kernel: the TMA-staged FLAT kernel for n in {2,4,8}
+    tma = os.environ.get("HFR_FLAT_TMA", "1") != "0" and n in (2, 4, 8)
+    kname = ("hfr_flat_tma_kernel" if tma else "hfr_flat_kernel") if args.algo == "flat" else "hfr_tree_kernel"
     if multi:
         nv_bytes = 2.0 * (n - 1) / n * S   # per GPU per direction per launch (§8d)
         roof = {"bound": "nvlink", "achieved": nv_bytes / t_step / 1e9, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
                 "frac": nv_bytes / t_step / 1e9 / NVLINK_PEER_GBS, "traffic": None,
-                "kernel": "hfr_flat_kernel" if args.algo == "flat" else "hfr_tree_kernel",
+                "kernel": kname,
                 "algorithmic_bytes_per_launch": nv_bytes,
                 "peak_source": "measured peer copy 770 GB/s/dir (B200_PROFILING.md); 900 nominal",
                 "frac_of_nominal": nv_bytes / t_step / 1e9 / NVLINK_NOMINAL_GBS}
@@ -313,7 +316,7 @@ def main():
         hbm_bytes = 2.0 * n * S            # every rank's buffer read once and written once
         roof = {"bound": "hbm", "achieved": hbm_bytes / t_step / 1e9, "peak": hbm_peak, "unit": "GB/s",
                 "frac": hbm_bytes / t_step / 1e9 / hbm_peak, "traffic": None,
-                "kernel": "hfr_flat_kernel" if args.algo == "flat" else "hfr_tree_kernel",
+                "kernel": kname,
                 "algorithmic_bytes_per_launch": hbm_bytes, "peak_source": hbm_src}
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
