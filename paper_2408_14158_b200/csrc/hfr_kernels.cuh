@@ -574,9 +574,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 constexpr int kTmaTileBytes = 4096;  // default bytes per source per stage (a.tma_tile)
 
-template <class E, int NR>
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+
+// BS: the results also leave through the bulk-copy engine (fold into a
+// shared-memory out stage, one cp.async.bulk store per destination rank).
+template <class E, int NR, bool BS>
 __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
-  extern __shared__ __align__(128) uint8_t stage_mem[];  // [2][NR][a.tma_tile]
+  extern __shared__ __align__(128) uint8_t stage_mem[];  // [2][NR][a.tma_tile] (+ BS: [2][a.tma_tile])
   __shared__ uint64_t bars[2];
   __shared__ uint64_t s_tile[2];
   const int rank = a.rank0 + blockIdx.y;
@@ -619,6 +627,12 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
       const uint64_t v0 = lo + t * TV;
       const uint64_t nv = v0 + TV < hi ? TV : hi - v0;
       const uint8_t* sm = stage_mem + (size_t)st * NR * TB;
+      uint8_t* out = stage_mem + (size_t)2 * NR * TB + (size_t)st * TB;
+      if constexpr (BS) {
+        // the bulk stores issued from out[st] two tiles ago have read it
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncthreads();
+      }
       for (uint64_t j = threadIdx.x; j < nv; j += blockDim.x) {
         float acc[K], tt[K];
         E::widen(*reinterpret_cast<const uint4*>(sm + j * 16), acc);
@@ -631,18 +645,36 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
 #pragma unroll
         for (int q = 0; q < K; ++q) acc[q] = __fmul_rn(acc[q], a.scale);
         const uint4 o = E::narrow(acc);
+        if constexpr (BS) {
+          *reinterpret_cast<uint4*>(out + j * 16) = o;
+        } else {
 #pragma unroll
-        for (int r = 0; r < NR; ++r)
-          if ((dmask >> r) & 1u) st128(a.buf[r] + (v0 + j) * 16, o);
+          for (int r = 0; r < NR; ++r)
+            if ((dmask >> r) & 1u) st128(a.buf[r] + (v0 + j) * 16, o);
+        }
       }
-      __syncthreads();  // every thread is done reading stage st
+      __syncthreads();  // every thread is done reading stage st (and writing out[st])
       if (threadIdx.x == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async-proxy refill
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem accesses before async proxy
+        if constexpr (BS) {
+#pragma unroll
+          for (int r = 0; r < NR; ++r)
+            if ((dmask >> r) & 1u) bulk_s2g(a.buf[r] + v0 * 16, out, (uint32_t)(nv * 16));
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
         const uint64_t tn = atomicAdd(ctr, 1ull);
         s_tile[st] = tn;
         if (tn < ntile) issue(st, tn);
       }
       __syncthreads();
+    }
+    if constexpr (BS) {
+      // every bulk store of this CTA has completed; make the async-proxy writes
+      // visible to generic accesses before the exit barrier's release
+      if (threadIdx.x == 0) {
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
     }
     // ragged tail (< K elements) — last rank, CTA 0
     const uint64_t t0 = nvec * K;

@@ -474,10 +474,11 @@ const void* flat_fn(int n) {
 
 template <class E>
 const void* flat_tma_fn(int n) {
+  static const bool bs = getenv("HFR_TMA_STORE") && strcmp(getenv("HFR_TMA_STORE"), "1") == 0;
   switch (n) {
-    case 2: return (const void*)hfr_flat_tma_kernel<E, 2>;
-    case 4: return (const void*)hfr_flat_tma_kernel<E, 4>;
-    case 8: return (const void*)hfr_flat_tma_kernel<E, 8>;
+    case 2: return bs ? (const void*)hfr_flat_tma_kernel<E, 2, true> : (const void*)hfr_flat_tma_kernel<E, 2, false>;
+    case 4: return bs ? (const void*)hfr_flat_tma_kernel<E, 4, true> : (const void*)hfr_flat_tma_kernel<E, 4, false>;
+    case 8: return bs ? (const void*)hfr_flat_tma_kernel<E, 8, true> : (const void*)hfr_flat_tma_kernel<E, 8, false>;
     default: return nullptr;
   }
 }
@@ -564,7 +565,8 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
   static const int tile = getenv("HFR_TMA_TILE") ? atoi(getenv("HFR_TMA_TILE")) : kTmaTileBytes;
   static const int per_sm = getenv("HFR_TMA_PER_SM") ? atoi(getenv("HFR_TMA_PER_SM")) : 2;
   const int threads = cta_threads(c, 256);
-  const int smem = 2 * c->n * tile;
+  static const bool bs = getenv("HFR_TMA_STORE") && strcmp(getenv("HFR_TMA_STORE"), "1") == 0;
+  const int smem = 2 * c->n * tile + (bs ? 2 * tile : 0);
   HFR_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : per_sm * c->num_sms;
   if (c->virt && c->local > 1) {
