@@ -122,6 +122,10 @@ typedef struct {
                              it (usable by every algo; required by NVLS).  Ignored for virtual comms.
                              If the box has no NVLS, init still succeeds and NVLS calls return
                              UNSUPPORTED.  0 (default): no arena. */
+    int flat_staging;     /* FLAT kernel staging: 0 auto (TMA bulk copies into shared memory for n in
+                             {2,4,8}, registers otherwise), 1 registers (no shared memory: small CTAs
+                             can share an SM with a compute kernel, e.g. DDP overlap), 2 TMA.  Bits
+                             are identical either way. */
 } hfr_config_t;
 
 /* Fill *cfg with the defaults above (algo AUTO, scale 1.0). */

@@ -57,7 +57,7 @@ class _Config(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int), ("chunk_elems", ctypes.c_size_t), ("max_ctas", ctypes.c_int),
                 ("threads", ctypes.c_int), ("scale", ctypes.c_float), ("scratch_bytes", ctypes.c_size_t),
                 ("timeout_ms", ctypes.c_int), ("oneshot_max_bytes", ctypes.c_size_t), ("stream_gate", ctypes.c_int),
-                ("nvls_bytes", ctypes.c_size_t)]
+                ("nvls_bytes", ctypes.c_size_t), ("flat_staging", ctypes.c_int)]
 
 
 @dataclass
@@ -73,13 +73,14 @@ class Config:
     oneshot_max_bytes: int = 0
     stream_gate: int = 0
     nvls_bytes: int = 0
+    flat_staging: int = 0
 
     def _c(self) -> _Config:
         if self.algo not in ALGOS:
             raise ValueError(f"unknown algo {self.algo!r}")
         return _Config(ALGOS[self.algo], self.chunk_elems, self.max_ctas, self.threads, self.scale,
                        self.scratch_bytes, self.timeout_ms, self.oneshot_max_bytes, self.stream_gate,
-                       self.nvls_bytes)
+                       self.nvls_bytes, self.flat_staging)
 
 
 _LIB = None

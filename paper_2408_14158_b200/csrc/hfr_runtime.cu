@@ -229,6 +229,7 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
   if (!(c.scale == c.scale)) return HFR_ERR_INVALID_ARGUMENT;
   if (c.timeout_ms < 0) return HFR_ERR_INVALID_ARGUMENT;
   if (c.stream_gate != 0 && c.stream_gate != 1) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.flat_staging < 0 || c.flat_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   return HFR_SUCCESS;
 }
 
@@ -598,9 +599,10 @@ hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
                       cudaStream_t s, int coll = HFR_ALLREDUCE, int root = 0, const Region* reg = nullptr,
                       uint64_t offset = 0) {
   // TMA-staged variant by default for n in {2,4,8} (r01: +2.5-4 % over the
-  // register-staged kernel; 99.5 % of HBM with 8 virtual ranks); HFR_FLAT_TMA=0
-  // selects the register-staged kernel
-  static const bool tma = !getenv("HFR_FLAT_TMA") || strcmp(getenv("HFR_FLAT_TMA"), "0") != 0;
+  // register-staged kernel; 98.5 % of HBM with 8 virtual ranks); config
+  // flat_staging (or HFR_FLAT_TMA=0/1 for A/B runs) overrides
+  const char* env = getenv("HFR_FLAT_TMA");
+  const bool tma = env ? strcmp(env, "0") != 0 : c->cfg.flat_staging != 1;
   if (tma && (coll == HFR_ALLREDUCE || coll == HFR_REDUCE_SCATTER)) {
 #define HFR_TMA_FN(E) flat_tma_fn<E>(c->n)
     const void* tfn = HFR_BY_DTYPE(dt, HFR_TMA_FN);

@@ -58,6 +58,7 @@ def main():
     ap.add_argument("--gate", type=int, default=0, help="hfr_config.stream_gate")
     ap.add_argument("--threads", type=int, default=0, help="threads per comm CTA (small CTAs can share an SM "
                                                           "with a GEMM CTA)")
+    ap.add_argument("--staging", type=int, default=0, help="hfr_config.flat_staging (1 = registers)")
     a = ap.parse_args()
 
     import torch
@@ -82,7 +83,8 @@ def main():
     numels = [o * i for _, o, i in params]
     nvls = (TOTAL * 2 + (256 << 20)) if a.algo == "nvls" else 0
     comm = hfr.Comm.init(device=local, config=hfr.Config(algo=a.algo, max_ctas=a.max_ctas, scale=1.0 / world,
-                                                        stream_gate=a.gate, nvls_bytes=nvls, threads=a.threads))
+                                                        stream_gate=a.gate, nvls_bytes=nvls, threads=a.threads,
+                                                        flat_staging=a.staging))
     ddp = HaiScaleDDP(comm, numels, torch.bfloat16, bucket_bytes=a.bucket_mib << 20)
     T = a.tokens
     g = torch.Generator(device=dev).manual_seed(3000 + rank)
@@ -145,7 +147,7 @@ def main():
         print(json.dumps({
             "config": "C5 HaiScale DDP", "n": n, "params": ddp.total, "grad_bytes": S,
             "buckets": len(ddp.bucket_ranges), "bucket_mib": a.bucket_mib, "max_ctas": a.max_ctas, "algo": a.algo,
-            "stream_gate": a.gate, "threads": a.threads, "side_priority": os.environ.get("HFR_SIDE_PRIORITY", "high"),
+            "stream_gate": a.gate, "threads": a.threads, "flat_staging": a.staging, "side_priority": os.environ.get("HFR_SIDE_PRIORITY", "high"),
             "tokens": T, "T_bwd_ms": tb * 1e3, "T_comm_ms": tc * 1e3, "T_both_ms": tt * 1e3,
             "overlap": (tb + tc - tt) / tc, "bwd_slowdown": tt / tb,
             "comm_busbw": S / tc * 2 * (n - 1) / n / 1e9, "bwd_tflops": flops / tb / 1e12,
