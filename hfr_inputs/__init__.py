@@ -98,3 +98,19 @@ C5_PARAMS = 7_000_000_000            # config 5: 7B bf16 gradient volume
 def c3_sizes_bytes() -> list[int]:
     """config 3: message sizes 1 KiB .. 1 GiB (powers of two)."""
     return [1024 << k for k in range(21)]
+
+
+def rank_input_torch(rank: int, count: int, dtype: str = FP32, seed_base: int = 7000, device="cuda"):
+    """Large seeded N(0,1) buffer generated on the device (torch.Generator
+    seeded with seed_base + rank), for full-size (1 GiB) cases whose host
+    generation would be slow.  Tests read sampled input elements back from the
+    device before the call and give those to the oracle."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed_base + rank)
+    x = torch.randn(count, generator=g, device=device, dtype=torch.float32)
+    if dtype == BF16:
+        return (x.view(torch.int32) >> 16).to(torch.int16).view(torch.bfloat16)  # truncation, as rank_input
+    if dtype == FP16:
+        return x.to(torch.float16)
+    return x

@@ -306,6 +306,13 @@ class Comm:
         self._allocs.append(ptrs[0])
         return out if self.virtual else out[0]
 
+    def free_all(self):
+        """Release every allocation made with empty() (COLLECTIVE); tensors
+        viewing them must not be used afterwards."""
+        for p in self._allocs:
+            _check(_lib().hfr_mem_free(self._h, ctypes.c_void_p(p)), "hfr_mem_free")
+        self._allocs = []
+
     def register(self, tensor):
         """Make a cudaMalloc'ed tensor peer visible (COLLECTIVE) for zero-copy."""
         _check(_lib().hfr_register(self._h, ctypes.c_void_p(tensor.data_ptr()),

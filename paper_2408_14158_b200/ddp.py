@@ -17,9 +17,10 @@ most SMs to the backward GEMMs (unlike the paper's copy-engine HFReduce,
 PAPER.md:375, an SM-driven allreduce is not free — DESIGN.md §6).
 
 Measured on 4 B200s with a 7e9-parameter LLaMA-shaped backward (C5): the
-best bit-exact setting is FLAT with Config(max_ctas=32, threads=128,
-stream_gate=1) — small comm CTAs share SMs with the GEMM CTAs — for an overlap
-of 0.86-0.89; algo "nvls" (order-relaxed) reaches 0.83-0.90.
+best bit-exact setting is FLAT with Config(max_ctas=24..32, threads=128,
+stream_gate=1, flat_staging=1) — small register-staged comm CTAs (no shared
+memory) share SMs with the GEMM CTAs — for an overlap of 0.85-0.89; algo
+"nvls" (order-relaxed) reaches 0.83-0.90.
 """
 from __future__ import annotations
 

@@ -72,6 +72,23 @@ def gpu_cases(rank, world, port, outdir):
                             res["ok"].append(name)
                         except AssertionError as e:
                             res["fail"].append(str(e)[:500])
+        # config 3's largest message (1 GiB bf16 per rank), FLAT, sampled check
+        comm.set_config(hfr.Config(algo="flat", scale=1.0 / world))
+        N = (1 << 30) // 2
+        t = comm.empty(N, torch.bfloat16)
+        t.copy_(gen.rank_input_torch(rank, N, gen.BF16, device=f"cuda:{rank}"))
+        idx = torch.from_numpy(np.random.default_rng(5).integers(0, N, size=1 << 19)).to(t.device)
+        col = to_numpy(t[idx])
+        cols = [None] * world
+        dist.all_gather_object(cols, col)
+        comm.allreduce(t)
+        torch.cuda.synchronize()
+        try:
+            assert_bit_exact(to_numpy(t[idx]), O.fold_ascending(cols, 1.0 / world), "1 GiB bf16 sampled")
+            res["ok"].append("1gib")
+        except AssertionError as e:
+            res["fail"].append(str(e)[:500])
+        del t
         # HaiScale DDP: bucketed async allreduce == fold of the arena
         from paper_2408_14158_b200.ddp import HaiScaleDDP
         comm.set_config(hfr.Config(algo="flat", scale=0.5))

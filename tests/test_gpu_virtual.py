@@ -155,6 +155,7 @@ def test_c2_full_size(hfr, algo):
         for o in outs[1:]:
             assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
         del outs, xs
+        comm_for(hfr, n).free_all()
 
 
 def test_bf16_exhaustive_n2_sample(hfr):
@@ -220,3 +221,41 @@ def test_collectives(hfr, n, dtype, kind, N):
             "allreduce": lambda: O.allreduce(xs, "flat", scale=0.5)}[kind]()
     for r, b in enumerate(bufs):
         assert_bit_exact(to_numpy(b), want[r], f"{kind} n={n} rank {r}")
+
+
+def test_c3_max_size_sampled(hfr):
+    """Config 3's largest message at the bench's launch configuration: 8
+    virtual ranks x 1 GiB bf16 (536,870,912 elements) with scale 1/8, FLAT
+    (TMA-staged) — 2^20 sampled outputs against the oracle on the sampled
+    input columns, and byte-identity of all 8 outputs."""
+    n, N = 8, (1 << 30) // 2
+    comm = comm_for(hfr, n)
+    comm.set_config(hfr.Config(algo="flat", scale=0.125))
+    bufs = comm.empty(N, torch.bfloat16)
+    for r, b in enumerate(bufs):
+        b.copy_(gen.rank_input_torch(r, N, gen.BF16, device="cuda:0"))
+    idx = torch.from_numpy(np.random.default_rng(5).integers(0, N, size=1 << 20)).cuda()
+    idx[:8] = torch.arange(N - 8, N, device="cuda")  # the ragged end
+    cols = [to_numpy(b[idx]) for b in bufs]
+    comm.allreduce_virtual(bufs)
+    torch.cuda.synchronize()
+    assert comm.status() == hfr.SUCCESS
+    want = O.fold_ascending(cols, 0.125)
+    for r, b in enumerate(bufs):
+        assert_bit_exact(to_numpy(b[idx]), want, f"1 GiB bf16 rank {r}")
+    h0 = bufs[0].view(torch.int16).sum(dtype=torch.int64)
+    for b in bufs[1:]:
+        assert torch.equal(b.view(torch.int16), bufs[0].view(torch.int16))
+    del bufs, h0
+    comm.free_all()
+
+
+def test_c2_bench_configuration(hfr):
+    """C2 exactly as bench.py times it: 8 virtual ranks x 186 MiB fp32,
+    gradient-like inputs (seeds 1000 + rank), FLAT, scale 1/8, symmetric
+    memory — every element bit-exact."""
+    n, N = 8, gen.C2_COUNT
+    xs = gen.rank_inputs(n, N, gen.FP32, "grad", seed_base=1000)
+    outs = run(hfr, n, xs, "flat", scale=1.0 / n)
+    check(outs, O.fold_ascending(xs, 1.0 / n), "C2 bench configuration")
+    comm_for(hfr, n).free_all()
