@@ -328,23 +328,49 @@ def main():
             pass
 
     # ---- e2e through the public API: H2D inputs, allreduce, D2H result ----
+    # The copies dominate (PCIe), so the step is pipelined the way a user of
+    # the public API would: the buffer is cut into 8 chunks; chunk i's H2D (one
+    # stream), allreduce (the current stream) and D2H (a third stream) overlap
+    # chunk i+1's.  Every byte of the inputs and of the result crosses PCIe
+    # inside the timed region.
     e2e = None
     if not args.no_e2e:
         host_out = [torch.empty_like(h).pin_memory() for h in host_in]
+        nchunk = 8
+        K = 8 if dtype == "bf16" else 4
+        edges = [(count * i // nchunk) // K * K for i in range(nchunk)] + [count]
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        ev_in = [torch.cuda.Event() for _ in range(nchunk)]
+        ev_red = [torch.cuda.Event() for _ in range(nchunk)]
 
         def e2e_step():
-            for b, h in zip(bufs, host_in):
-                b.copy_(h, non_blocking=True)
-            step()
-            for b, o in zip(bufs, host_out):
-                o.copy_(b, non_blocking=True)
+            cur = torch.cuda.current_stream()
+            s_in.wait_stream(cur)
+            for i in range(nchunk):
+                lo, hi = edges[i], edges[i + 1]
+                with torch.cuda.stream(s_in):
+                    for b, h in zip(bufs, host_in):
+                        b[lo:hi].copy_(h[lo:hi], non_blocking=True)
+                    ev_in[i].record(s_in)
+                cur.wait_event(ev_in[i])
+                if multi:
+                    comm.allreduce(bufs[0][lo:hi])
+                else:
+                    comm.allreduce_virtual([b[lo:hi] for b in bufs])
+                ev_red[i].record(cur)
+                s_out.wait_event(ev_red[i])
+                with torch.cuda.stream(s_out):
+                    for b, o in zip(bufs, host_out):
+                        o[lo:hi].copy_(b[lo:hi], non_blocking=True)
+            cur.wait_stream(s_out)
 
         e2e_step()
         torch.cuda.synchronize()
-        t_e2e, _ = timed(e2e_step, max(1, min(args.steps, 10)))
+        t_e2e, e2e_launches = timed(e2e_step, max(1, min(args.steps, 10)))
         e2e = {"value": busbw(S, t_e2e, n), "unit": "GB/s", "ms_per_step": t_e2e * 1e3,
                "h2d_bytes_per_step": S * len(bufs), "d2h_bytes_per_step": S * len(bufs),
-               "note": "per step: pinned H2D of each local rank's input, hfr_allreduce, D2H of the result"}
+               "note": "per step: pinned H2D of each local rank's input, hfr_allreduce, D2H of the result, "
+                       "pipelined over 8 chunks on 3 streams"}
 
     # ---- context: NCCL on the same buffer, and the tree schedules ----
     nccl = None
