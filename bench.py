@@ -53,6 +53,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-nccl", action="store_true")
     p.add_argument("--no-variants", action="store_true")
+    p.add_argument("--e2e-chunks", type=int, default=8, help="pipeline depth of the e2e step (1 = sequential)")
     return p.parse_args()
 
 
@@ -336,7 +337,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         host_out = [torch.empty_like(h).pin_memory() for h in host_in]
-        nchunk = 8
+        nchunk = max(1, args.e2e_chunks)
         K = 8 if dtype == "bf16" else 4
         edges = [(count * i // nchunk) // K * K for i in range(nchunk)] + [count]
         s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
@@ -370,7 +371,7 @@ def main():
         e2e = {"value": busbw(S, t_e2e, n), "unit": "GB/s", "ms_per_step": t_e2e * 1e3,
                "h2d_bytes_per_step": S * len(bufs), "d2h_bytes_per_step": S * len(bufs),
                "note": "per step: pinned H2D of each local rank's input, hfr_allreduce, D2H of the result, "
-                       "pipelined over 8 chunks on 3 streams"}
+                       f"pipelined over {nchunk} chunk(s) on 3 streams"}
 
     # ---- context: NCCL on the same buffer, and the tree schedules ----
     nccl = None
