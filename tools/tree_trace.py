@@ -104,7 +104,7 @@ def main():
     torch.cuda.synchronize()
     comm.set_trace(None)
     os.makedirs(a.out, exist_ok=True)
-    arr = tb.view(torch.int64).view(1024, cap, 8)[: (a.ctas or 148)].cpu().numpy().view(np.uint64)
+    arr = tb.view(torch.int64).view(1024, cap, 8)[: (a.ctas or 296)].cpu().numpy().view(np.uint64)
     np.save(os.path.join(a.out, f"rank{rank}.npy"), arr)
     ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
