@@ -1049,6 +1049,74 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
   auto member = [&](int node) { return PAIR ? 2 * node + h : node; };
 
   Tracer tr(a);
+  __shared__ int s_ready;
+  // Down pass of chunk c (Alg. 2 pass 2): wait for (block) or poll (!block)
+  // the final chunk from the parent, then forward it to the children (and the
+  // pair partner).  Returns 1 done, 0 not ready yet, -1 error.
+  auto down_chunk = [&](uint64_t c, bool block) -> int {
+    const TreeNode nd = a.tree[c & 1][me];
+    if (nd.parent < 0) return 1;  // the root already pushed its final chunk in the up pass
+    const uint32_t lc = (uint32_t)(c - a.c_lo);
+    const uint64_t tw = tr.p ? globaltimer() : 0;
+    if (threadIdx.x == 0) {
+      if (block)
+        s_ready = wait_ge(a, &mypad->down[lc], ep) ? 1 : -1;
+      else
+        s_ready = ld_acquire_sys(&mypad->down[lc]) >= ep ? 1 : 0;
+    }
+    __syncthreads();
+    const int ready = s_ready;
+    __syncthreads();
+    if (ready != 1) return ready;
+    const uint64_t tk = tr.p ? globaltimer() : 0;
+    if (nd.nchild == 0 && !PAIR) {
+      if (threadIdx.x == 0) tr.rec((2ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, tk, tk);
+      return 1;
+    }
+    const uint64_t e0 = c * C, e1 = (e0 + C < len) ? e0 + C : len;
+    const int esz = (int)sizeof(typename E::T);
+    const uint64_t b0 = (base + e0) * esz, b1 = (base + e1) * esz;  // byte range
+    const uint64_t nv = (b1 - b0) / 16;
+    constexpr int DU = 4;  // 4 x 16 B loads in flight per thread before the stores
+    for (uint64_t v0 = threadIdx.x; v0 < nv; v0 += (uint64_t)blockDim.x * DU) {
+      uint4 val[DU];
+#pragma unroll
+      for (int u = 0; u < DU; ++u)
+        if (v0 + (uint64_t)u * blockDim.x < nv) val[u] = ld128(mybuf + b0 + (v0 + (uint64_t)u * blockDim.x) * 16);
+#pragma unroll
+      for (int u = 0; u < DU; ++u) {
+        if (v0 + (uint64_t)u * blockDim.x >= nv) break;
+        const uint64_t off = b0 + (v0 + (uint64_t)u * blockDim.x) * 16;
+        for (int k = 0; k < nd.nchild; ++k) st128(a.buf[member(nd.child[k])] + off, val[u]);
+        if constexpr (PAIR) st128(a.buf[partner] + off, val[u]);
+      }
+    }
+    for (uint64_t y = b0 + nv * 16 + threadIdx.x * esz; y < b1; y += (uint64_t)blockDim.x * esz) {
+      if (esz == 2) {
+        const uint16_t val = *reinterpret_cast<const uint16_t*>(mybuf + y);
+        for (int k = 0; k < nd.nchild; ++k) *reinterpret_cast<uint16_t*>(a.buf[member(nd.child[k])] + y) = val;
+        if constexpr (PAIR) *reinterpret_cast<uint16_t*>(a.buf[partner] + y) = val;
+      } else {
+        const uint32_t val = *reinterpret_cast<const uint32_t*>(mybuf + y);
+        for (int k = 0; k < nd.nchild; ++k) *reinterpret_cast<uint32_t*>(a.buf[member(nd.child[k])] + y) = val;
+        if constexpr (PAIR) *reinterpret_cast<uint32_t*>(a.buf[partner] + y) = val;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint64_t ts = tr.p ? globaltimer() : 0;
+      fence_acq_rel_sys();
+      for (int k = 0; k < nd.nchild; ++k) st_relaxed_sys(&a.pad[member(nd.child[k])]->down[lc], ep);
+      if constexpr (PAIR) st_relaxed_sys(&a.pad[partner]->pdown[lc], ep);
+      tr.rec((2ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, ts, globaltimer());
+    }
+    return 1;
+  };
+  // next chunk whose down pass is pending: down passes are interleaved with
+  // the up passes as soon as their final chunk arrives, so a rank's ingress
+  // and egress are spread over the whole launch instead of up-then-down
+  uint64_t dn = a.c_lo + b;
+
   // ---- up pass -----------------------------------------------------------
   for (uint64_t c = a.c_lo + b; c < c_end; c += gridDim.x) {
     const TreeNode nd = a.tree[c & 1][me];
@@ -1205,60 +1273,18 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
       }
       tr.rec((1ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, ts, globaltimer());
     }
+    // opportunistic down passes (non-blocking)
+    while (dn <= c) {
+      const int r = down_chunk(dn, false);
+      if (r < 0) return;
+      if (r == 0) break;
+      dn += gridDim.x;
+    }
   }
 
-  // ---- down pass ---------------------------------------------------------
-  for (uint64_t c = a.c_lo + b; c < c_end; c += gridDim.x) {
-    const TreeNode nd = a.tree[c & 1][me];
-    if (nd.parent < 0) continue;  // the root already pushed its final chunk
-    const uint32_t lc = (uint32_t)(c - a.c_lo);
-    const uint64_t tw = tr.p ? globaltimer() : 0;
-    bool got = true;
-    if (threadIdx.x == 0) got = wait_ge(a, &mypad->down[lc], ep);
-    if (!__syncthreads_and(got)) return;
-    const uint64_t tk = tr.p ? globaltimer() : 0;
-    if (nd.nchild == 0 && !PAIR) {
-      tr.rec((2ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, tk, tk);
-      continue;
-    }
-    const uint64_t e0 = c * C, e1 = (e0 + C < len) ? e0 + C : len;
-    const int esz = (int)sizeof(typename E::T);
-    const uint64_t b0 = (base + e0) * esz, b1 = (base + e1) * esz;  // byte range
-    const uint64_t nv = (b1 - b0) / 16;
-    constexpr int DU = 4;  // 4 x 16 B loads in flight per thread before the stores
-    for (uint64_t v0 = threadIdx.x; v0 < nv; v0 += (uint64_t)blockDim.x * DU) {
-      uint4 val[DU];
-#pragma unroll
-      for (int u = 0; u < DU; ++u)
-        if (v0 + (uint64_t)u * blockDim.x < nv) val[u] = ld128(mybuf + b0 + (v0 + (uint64_t)u * blockDim.x) * 16);
-#pragma unroll
-      for (int u = 0; u < DU; ++u) {
-        if (v0 + (uint64_t)u * blockDim.x >= nv) break;
-        const uint64_t off = b0 + (v0 + (uint64_t)u * blockDim.x) * 16;
-        for (int k = 0; k < nd.nchild; ++k) st128(a.buf[member(nd.child[k])] + off, val[u]);
-        if constexpr (PAIR) st128(a.buf[partner] + off, val[u]);
-      }
-    }
-    for (uint64_t y = b0 + nv * 16 + threadIdx.x * esz; y < b1; y += (uint64_t)blockDim.x * esz) {
-      if (esz == 2) {
-        const uint16_t val = *reinterpret_cast<const uint16_t*>(mybuf + y);
-        for (int k = 0; k < nd.nchild; ++k) *reinterpret_cast<uint16_t*>(a.buf[member(nd.child[k])] + y) = val;
-        if constexpr (PAIR) *reinterpret_cast<uint16_t*>(a.buf[partner] + y) = val;
-      } else {
-        const uint32_t val = *reinterpret_cast<const uint32_t*>(mybuf + y);
-        for (int k = 0; k < nd.nchild; ++k) *reinterpret_cast<uint32_t*>(a.buf[member(nd.child[k])] + y) = val;
-        if constexpr (PAIR) *reinterpret_cast<uint32_t*>(a.buf[partner] + y) = val;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const uint64_t ts = tr.p ? globaltimer() : 0;
-      fence_acq_rel_sys();
-      for (int k = 0; k < nd.nchild; ++k) st_relaxed_sys(&a.pad[member(nd.child[k])]->down[lc], ep);
-      if constexpr (PAIR) st_relaxed_sys(&a.pad[partner]->pdown[lc], ep);
-      tr.rec((2ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, ts, globaltimer());
-    }
-  }
+  // ---- down pass: the rest (blocking) -------------------------------------
+  for (; dn < c_end; dn += gridDim.x)
+    if (down_chunk(dn, true) < 0) return;
 
   // ---- PAIR: wait until the partner's half has fully landed in my buffer ---
   if constexpr (PAIR) {
