@@ -81,6 +81,7 @@ struct Args {
   uint32_t dst_mask;       // FLAT kernel: ranks that receive the result (0 = the owner itself)
   int dyn_tiles;           // FLAT kernel: warps grab tiles from a per-rank counter (no tail imbalance)
   int tma_tile;            // FLAT TMA kernel: bytes per source per stage (multiple of 16)
+  int tree_interleave;     // tree kernels: interleave down passes with up passes
   int excl_root;           // FLAT kernel: >= 0: this rank owns no shard (reduce/broadcast root)
   char* mcbuf;              // NVLS: multicast VA of this call's buffer
   uint32_t* mc_exit;       // NVLS: multicast VA of the exit counters [kMaxCtas]
@@ -1274,7 +1275,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
       tr.rec((1ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, ts, globaltimer());
     }
     // opportunistic down passes (non-blocking)
-    while (dn <= c) {
+    while (a.tree_interleave && dn <= c) {
       const int r = down_chunk(dn, false);
       if (r < 0) return;
       if (r == 0) break;

@@ -662,6 +662,8 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   }
   fill_tree_nodes(a.ntree, a.tree);
   a.chunk = (int)C;
+  static const bool interleave = getenv("HFR_TREE_INTERLEAVE") && strcmp(getenv("HFR_TREE_INTERLEAVE"), "1") == 0;
+  a.tree_interleave = interleave ? 1 : 0;
   for (int q = 0; q < c->n; ++q) {
     a.buf[q] = bufs[q];
     a.part[q] = reinterpret_cast<float*>(stage_base(c, q) + stage);
