@@ -111,8 +111,9 @@ typedef struct {
     float scale;          /* gradient scale, multiplies the fp32 total once (reading R3); 1.0 = sum */
     size_t scratch_bytes; /* per-rank library scratch (staging + tree partials); 0 -> 256 MiB */
     int timeout_ms;       /* cross-rank spin-wait timeout; 0 -> 60000 */
-    size_t oneshot_max_bytes; /* largest message for ONESHOT (and AUTO's switch point); fixed at
-                                 init (sizes the per-rank inbox: 2 * nranks * this); 0 -> 512 KiB */
+    size_t oneshot_max_bytes; /* largest message for an explicit ONESHOT (AUTO switches at 64 KiB);
+                                 fixed at init (sizes the per-rank inbox: 2 * nranks * this);
+                                 0 -> 512 KiB */
     int stream_gate;      /* 1: before launching an SM schedule, make the stream wait (stream memory
                              operations in the copy-engine front end, no SM) until every rank has
                              reached this call, so no CTA spins on a late peer (overlap with compute);
@@ -147,9 +148,9 @@ hfr_status_t hfr_init(hfr_comm_t* comm, int rank, int nranks, int cuda_device,
  * used for the 1-GPU bench line and the 1-GPU parity tests. */
 hfr_status_t hfr_init_virtual(hfr_comm_t* comm, int nranks, int cuda_device, const hfr_config_t* cfg);
 
-/* COLLECTIVE.  Change algo / scale / chunk_elems / max_ctas / threads for
- * subsequent calls (scratch_bytes, timeout_ms and oneshot_max_bytes are fixed
- * at init). */
+/* COLLECTIVE.  Change the configuration for subsequent calls
+ * (scratch_bytes, timeout_ms, oneshot_max_bytes and nvls_bytes are fixed at
+ * init and keep their init values). */
 hfr_status_t hfr_comm_set_config(hfr_comm_t comm, const hfr_config_t* cfg);
 
 /* Number of ranks this process drives: 1 for hfr_init comms, nranks for
@@ -163,6 +164,9 @@ int hfr_comm_nranks(hfr_comm_t comm);
  * Buffers inside such memory are reduced zero-copy (no staging).  Freed by
  * hfr_mem_free (collective) or hfr_finalize. */
 hfr_status_t hfr_mem_alloc(hfr_comm_t comm, size_t bytes, void** ptrs);
+/* COLLECTIVE.  Release an hfr_mem_alloc allocation (ptr = the first pointer
+ * hfr_mem_alloc returned).  Memory inside the NVLS arena is released only by
+ * hfr_finalize (SUCCESS, no-op).  INVALID_ARGUMENT for unknown pointers. */
 hfr_status_t hfr_mem_free(hfr_comm_t comm, void* ptr);
 
 /* COLLECTIVE.  Make an existing cudaMalloc'ed range [ptr, ptr+bytes) peer
