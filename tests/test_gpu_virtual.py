@@ -259,3 +259,31 @@ def test_c2_bench_configuration(hfr):
     outs = run(hfr, n, xs, "flat", scale=1.0 / n)
     check(outs, O.fold_ascending(xs, 1.0 / n), "C2 bench configuration")
     comm_for(hfr, n).free_all()
+
+
+_FUZZ = np.random.default_rng(20261018)
+_FUZZ_CASES = []
+for _i in range(48):
+    _n = int(_FUZZ.integers(1, 9))
+    _algo = str(_FUZZ.choice(["flat", "oneshot", "dbt", "pair_dbt", "auto", "ce"]))
+    if _algo == "pair_dbt" and _n % 2:
+        _n += 1 if _n < 8 else -1
+    _FUZZ_CASES.append(dict(
+        n=_n, algo=_algo, dtype=str(_FUZZ.choice([gen.FP32, gen.BF16, gen.FP16])),
+        count=int(_FUZZ.choice([int(_FUZZ.integers(0, 64)), int(_FUZZ.integers(64, 20_000)),
+                                int(_FUZZ.integers(20_000, 400_000))])),
+        chunk=256 * int(_FUZZ.integers(1, 33)), scale=float(_FUZZ.choice([1.0, 0.5, 1.0 / 3, 2.0])),
+        mem=str(_FUZZ.choice(["symmetric", "plain", "offset"])), async_op=bool(_FUZZ.integers(0, 2)),
+        dist=str(_FUZZ.choice(["normal", "loguniform", "specials", "int"])), seed=int(_FUZZ.integers(0, 1 << 30))))
+
+
+@pytest.mark.parametrize("case", _FUZZ_CASES, ids=lambda c: f"{c['algo']}-n{c['n']}-{c['dtype']}-{c['count']}-{c['mem']}")
+def test_fuzz_configs(hfr, case):
+    """Seeded random configurations (rank count, schedule, dtype, size, chunk,
+    scale, memory kind, sync/async, value mix), each bit-exact vs the oracle."""
+    c = case
+    xs = gen.rank_inputs(c["n"], c["count"], c["dtype"], c["dist"], seed_base=c["seed"])
+    outs = run(hfr, c["n"], xs, c["algo"], chunk=c["chunk"], scale=c["scale"],
+               symmetric=c["mem"] != "plain", offset=1 if c["mem"] == "offset" else 0, async_op=c["async_op"])
+    want = O.allreduce(xs, c["algo"], chunk_elems=c["chunk"], scale=c["scale"])[0]
+    check(outs, want, str(c))
