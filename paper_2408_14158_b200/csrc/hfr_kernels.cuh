@@ -592,12 +592,15 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
   const int b = blockIdx.x;
   const uint64_t e = begin_epoch(a.pad[rank]);
   const uint32_t dmask = a.dst_mask ? a.dst_mask : (1u << rank);
-  if (entry_barrier(a, rank, b, e)) {
+  // shard owners: all ranks, or (reduce) the n-1 ranks other than the root
+  const int nown = a.excl_root >= 0 ? NR - 1 : NR;
+  const int own = a.excl_root >= 0 ? (rank < a.excl_root ? rank : rank - 1) : rank;
+  if (entry_barrier(a, rank, b, e) && rank != a.excl_root) {
     constexpr int K = E::kPerVec;
     const uint64_t TB = (uint64_t)a.tma_tile;    // bytes per source per stage
     const uint64_t TV = TB / 16;                 // vectors per tile
     const uint64_t nvec = a.count / K;
-    const uint64_t lo = nvec * rank / NR, hi = nvec * (rank + 1) / NR;
+    const uint64_t lo = nvec * own / nown, hi = nvec * (own + 1) / nown;
     const uint64_t ntile = (hi - lo + TV - 1) / TV;
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(&a.pad[rank]->tile_next);
     auto issue = [&](int st, uint64_t t) {  // thread 0 only
@@ -677,9 +680,9 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
         asm volatile("fence.proxy.async.global;" ::: "memory");
       }
     }
-    // ragged tail (< K elements) — last rank, CTA 0
+    // ragged tail (< K elements) — last owner, CTA 0
     const uint64_t t0 = nvec * K;
-    if (rank == NR - 1 && b == 0 && threadIdx.x < a.count - t0) {
+    if (own == nown - 1 && b == 0 && threadIdx.x < a.count - t0) {
       const uint64_t el = t0 + threadIdx.x;
       float acc = E::load1(a.buf[0], el);
       for (int r = 1; r < NR; ++r) acc = __fadd_rn(acc, E::load1(a.buf[r], el));

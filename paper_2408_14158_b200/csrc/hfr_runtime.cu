@@ -559,7 +559,7 @@ void coll_routing(const hfr_comm_s* c, int coll, int root, int* src, uint32_t* d
   }
 }
 
-// TMA-staged FLAT (default for allreduce / reduce-scatter with n in {2, 4, 8})
+// TMA-staged FLAT (default for allreduce / reduce-scatter / reduce with n in {2, 4, 8})
 hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                           cudaStream_t s, int coll, int root, const void* fn) {
   // experiment knobs: HFR_TMA_TILE (bytes per source per stage), HFR_TMA_PER_SM
@@ -580,8 +580,7 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
   base_args(c, a, count, fnv(fnv(sig, 0x544d41), (uint64_t)g * 1315423911ull + threads));
   for (int q = 0; q < c->n; ++q) a.buf[q] = bufs[q];
   a.tma_tile = tile;
-  int excl = -1;
-  coll_routing(c, coll, root, &a.src_rank, &a.dst_mask, &excl);
+  coll_routing(c, coll, root, &a.src_rank, &a.dst_mask, &a.excl_root);
   ++c->epoch;
   void* params[] = {&a};
   cudaError_t e = (c->virt && c->local > 1)
@@ -603,7 +602,7 @@ hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   // flat_staging (or HFR_FLAT_TMA=0/1 for A/B runs) overrides
   const char* env = getenv("HFR_FLAT_TMA");
   const bool tma = env ? strcmp(env, "0") != 0 : c->cfg.flat_staging != 1;
-  if (tma && (coll == HFR_ALLREDUCE || coll == HFR_REDUCE_SCATTER)) {
+  if (tma && (coll == HFR_ALLREDUCE || coll == HFR_REDUCE_SCATTER || coll == HFR_REDUCE)) {
 #define HFR_TMA_FN(E) flat_tma_fn<E>(c->n)
     const void* tfn = HFR_BY_DTYPE(dt, HFR_TMA_FN);
     if (tfn) return run_flat_tma(c, bufs, count, dt, sig, s, coll, root, tfn);
