@@ -574,6 +574,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 constexpr int kTmaTileBytes = 4096;  // default bytes per source per stage (a.tma_tile)
+constexpr uint64_t kPairSubUnits = 256;  // PAIR tree kernel: 8-element units per partner sub-tile
 
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
@@ -1116,6 +1117,18 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     }
     return 1;
   };
+  // PAIR: 2-stage shared-memory ring for the partner's chunk (bulk copies)
+  __shared__ __align__(128) uint8_t pstage[PAIR ? 2 * kPairSubUnits * 8 * sizeof(typename E::T) : 16];
+  __shared__ uint64_t pbar[2];
+  uint32_t puse[2] = {0, 0};
+  if constexpr (PAIR) {
+    if (threadIdx.x == 0) {
+      mbar_init(&pbar[0], 1);
+      mbar_init(&pbar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
   // next chunk whose down pass is pending: down passes are interleaved with
   // the up passes as soon as their final chunk arrives, so a rank's ingress
   // and egress are spread over the whole launch instead of up-then-down
@@ -1126,6 +1139,22 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     const TreeNode nd = a.tree[c & 1][me];
     const uint32_t lc = (uint32_t)(c - a.c_lo);
     const uint64_t tw = tr.p ? globaltimer() : 0;
+    // PAIR: start pulling the partner's chunk before waiting on the children
+    const uint64_t pe0 = c * C, pe1 = (pe0 + C < len) ? pe0 + C : len;
+    const uint64_t nsub = ((pe1 - pe0) / 8 + kPairSubUnits - 1) / kPairSubUnits;
+    auto pair_issue = [&](int st, uint64_t j) {  // thread 0 only
+      constexpr uint64_t esz = sizeof(typename E::T);
+      const uint64_t nvc = (pe1 - pe0) / 8;
+      const uint64_t u0 = j * kPairSubUnits, u1 = u0 + kPairSubUnits < nvc ? u0 + kPairSubUnits : nvc;
+      const uint32_t bytes = (uint32_t)((u1 - u0) * 8 * esz);
+      mbar_expect_tx(&pbar[st], bytes);
+      bulk_g2s(pstage + (size_t)st * kPairSubUnits * 8 * esz, a.buf[partner] + (base + pe0 + u0 * 8) * esz, bytes,
+               &pbar[st]);
+    };
+    if constexpr (PAIR) {
+      if (threadIdx.x == 0)
+        for (uint64_t j = 0; j < 2 && j < nsub; ++j) pair_issue((int)j, j);
+    }
     bool got = true;
     if (threadIdx.x < nd.nchild) got = wait_ge(a, &mypad->up[threadIdx.x][lc], ep);
     if (!__syncthreads_and(got)) return;
@@ -1136,10 +1165,6 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     const bool root = nd.parent < 0;
     char* const pbuf = PAIR ? a.buf[partner] : nullptr;
     float* const dst_part = root ? nullptr : a.part[member(nd.parent)] + (uint64_t)nd.slot * a.part_stride;
-    // TU units of 8 elements per thread per iteration: every load of the TU
-    // units (x_v, the partner's x, the children's partials) is issued before
-    // the first add, so a CTA keeps TU x (2..4) x 32 B per thread in flight.
-    constexpr int TU = 1;
     const int nchild = nd.nchild, self_pos = nd.self_pos;
     // A DBT leaf's partial is its own x: stream it as a copy with 4 x 16 B in
     // flight per thread (r01: DBT n=4 313 -> 360-378 GB/s).  bf16 leaves send
@@ -1183,59 +1208,72 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
         }
       }
     }
-    for (uint64_t v0 = leafcopy ? nv : threadIdx.x; v0 < nv; v0 += (uint64_t)blockDim.x * TU) {
-      float xv[TU][8], pp[TU][2][8];
-      bool okv[TU];
+    // one unit = 8 elements at offset e of the half; xp = the pair partner's
+    // 8 values (PAIR, staged in shared memory) or nullptr
+    auto unit = [&](uint64_t v, const float* xp) {
+      const uint64_t e = e0 + v * 8;
+      float xv[8], pp[2][8];
+      load8<E>(mybuf, base + e, xv);
+      if constexpr (PAIR) {
+        // node value x_v = fl32(x_2k + x_2k+1), lower rank first
 #pragma unroll
-      for (int u = 0; u < TU; ++u) okv[u] = v0 + (uint64_t)u * blockDim.x < nv;
+        for (int k = 0; k < 8; ++k) xv[k] = h == 0 ? __fadd_rn(xv[k], xp[k]) : __fadd_rn(xp[k], xv[k]);
+      }
 #pragma unroll
-      for (int u = 0; u < TU; ++u) {
-        if (!okv[u]) continue;
-        const uint64_t e = e0 + (v0 + (uint64_t)u * blockDim.x) * 8;
-        load8<E>(mybuf, base + e, xv[u]);
-        if constexpr (PAIR) {
+      for (int sl = 0; sl < 2; ++sl)
+        if (sl < nchild) {
+          if (E::kPerVec == 8 && slot_bf16[sl])
+            load8<E>(reinterpret_cast<const char*>(mypart + (uint64_t)sl * a.part_stride + e0), e - e0, pp[sl]);
+          else
+            load8_f32(mypart + (uint64_t)sl * a.part_stride, e, pp[sl]);
+        }
+      // in-order combination: children below, x_v, children above (R10)
+      float acc[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = self_pos == 0 ? xv[j] : pp[0][j];
+#pragma unroll
+      for (int k = 1; k <= 2; ++k) {
+        if (k > nchild) break;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float t = k == self_pos ? xv[j] : (k < self_pos ? pp[k][j] : pp[k - 1][j]);
+          acc[j] = __fadd_rn(acc[j], t);
+        }
+      }
+      if (root) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = __fmul_rn(acc[j], a.scale);
+        store8<E>(mybuf, base + e, acc);
+        for (int k = 0; k < nchild; ++k) store8<E>(a.buf[member(nd.child[k])], base + e, acc);
+        if constexpr (PAIR) store8<E>(pbuf, base + e, acc);
+      } else {
+        store8_f32(dst_part, e, acc);
+      }
+    };
+    if constexpr (PAIR) {
+      // the partner's chunk arrives through the bulk-copy engine, sub-tile by
+      // sub-tile into a 2-stage ring (prefetched before the children's wait)
+      constexpr uint64_t esz = sizeof(typename E::T);
+      for (uint64_t j = 0; j < nsub; ++j) {
+        const int st = (int)(j & 1);
+        mbar_wait(&pbar[st], puse[st] & 1);
+        ++puse[st];
+        const uint64_t u0 = j * kPairSubUnits, u1 = u0 + kPairSubUnits < nv ? u0 + kPairSubUnits : nv;
+        const uint8_t* sm = pstage + (size_t)st * kPairSubUnits * 8 * esz;
+        for (uint64_t v = u0 + threadIdx.x; v < u1; v += blockDim.x) {
           float xp[8];
-          load8<E>(pbuf, base + e, xp);
-          // node value x_v = fl32(x_2k + x_2k+1), lower rank first
-#pragma unroll
-          for (int k = 0; k < 8; ++k) xv[u][k] = h == 0 ? __fadd_rn(xv[u][k], xp[k]) : __fadd_rn(xp[k], xv[u][k]);
+          E::widen(*reinterpret_cast<const uint4*>(sm + (v - u0) * 8 * esz), xp);
+          if constexpr (esz == 4) E::widen(*reinterpret_cast<const uint4*>(sm + (v - u0) * 32 + 16), xp + 4);
+          unit(v, xp);
         }
-#pragma unroll
-        for (int sl = 0; sl < 2; ++sl)
-          if (sl < nchild) {
-            if (E::kPerVec == 8 && slot_bf16[sl])
-              load8<E>(reinterpret_cast<const char*>(mypart + (uint64_t)sl * a.part_stride + e0), e - e0, pp[u][sl]);
-            else
-              load8_f32(mypart + (uint64_t)sl * a.part_stride, e, pp[u][sl]);
-          }
-      }
-#pragma unroll
-      for (int u = 0; u < TU; ++u) {
-        if (!okv[u]) continue;
-        const uint64_t e = e0 + (v0 + (uint64_t)u * blockDim.x) * 8;
-        // in-order combination: children below, x_v, children above (R10)
-        float acc[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = self_pos == 0 ? xv[u][j] : pp[u][0][j];
-#pragma unroll
-        for (int k = 1; k <= 2; ++k) {
-          if (k > nchild) break;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float t = k == self_pos ? xv[u][j] : (k < self_pos ? pp[u][k][j] : pp[u][k - 1][j]);
-            acc[j] = __fadd_rn(acc[j], t);
-          }
-        }
-        if (root) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] = __fmul_rn(acc[j], a.scale);
-          store8<E>(mybuf, base + e, acc);
-          for (int k = 0; k < nchild; ++k) store8<E>(a.buf[member(nd.child[k])], base + e, acc);
-          if constexpr (PAIR) store8<E>(pbuf, base + e, acc);
-        } else {
-          store8_f32(dst_part, e, acc);
+        __syncthreads();  // stage st consumed
+        if (threadIdx.x == 0 && j + 2 < nsub) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          pair_issue(st, j + 2);
         }
       }
+    } else {
+      for (uint64_t v = leafcopy ? nv : threadIdx.x; v < nv; v += blockDim.x) unit(v, nullptr);
     }
     // ragged tail of the half (only the last chunk can have one)
     for (uint64_t e = e0 + nv * 8 + threadIdx.x; e < e1; e += blockDim.x) {
