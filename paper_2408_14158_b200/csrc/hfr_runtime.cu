@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/hfr.h"
@@ -568,7 +569,11 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
   const int threads = cta_threads(c, 256);
   static const bool bs = getenv("HFR_TMA_STORE") && strcmp(getenv("HFR_TMA_STORE"), "1") == 0;
   const int smem = 2 * c->n * tile + (bs ? 2 * tile : 0);
-  HFR_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  static std::vector<std::pair<const void*, int>> smem_set;  // (kernel, bytes) already configured
+  if (std::find(smem_set.begin(), smem_set.end(), std::make_pair(fn, smem)) == smem_set.end()) {
+    HFR_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    smem_set.emplace_back(fn, smem);
+  }
   int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : per_sm * c->num_sms;
   if (c->virt && c->local > 1) {
     int occ = 0;
