@@ -575,6 +575,10 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
     smem_set.emplace_back(fn, smem);
   }
   int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : per_sm * c->num_sms;
+  // no more CTAs than tiles: idle CTAs would only add handshakes
+  const uint64_t per = dt == HFR_FLOAT32 ? 4 : 8;
+  const uint64_t tiles = (count / per / c->n + (uint64_t)tile / 16 - 1) / ((uint64_t)tile / 16) + 1;
+  g = (int)std::min<uint64_t>((uint64_t)g, tiles);
   if (c->virt && c->local > 1) {
     int occ = 0;
     HFR_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
