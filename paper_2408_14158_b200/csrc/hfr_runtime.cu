@@ -694,7 +694,11 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   return HFR_SUCCESS;
 }
 
-constexpr uint64_t kLLMaxBytes = 64u << 10;  // ONESHOT uses the LL (flag-in-data) form up to here
+// ONESHOT uses the LL (flag-in-data) form up to here (env HFR_LL_MAX for sweeps)
+uint64_t ll_max_bytes() {
+  static const uint64_t v = getenv("HFR_LL_MAX") ? strtoull(getenv("HFR_LL_MAX"), nullptr, 10) : (64u << 10);
+  return v;
+}
 
 hfr_status_t run_oneshot_ll(hfr_comm_s* c, char* const* local_bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                             cudaStream_t s) {
@@ -725,7 +729,7 @@ hfr_status_t run_oneshot_ll(hfr_comm_s* c, char* const* local_bufs, uint64_t cou
 hfr_status_t run_oneshot(hfr_comm_s* c, char* const* local_bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                          cudaStream_t s) {
   // LL form: 8 inbox bytes per element, one NVLink write of latency
-  if (count * dtype_size(dt) <= kLLMaxBytes && count * 8 <= c->cfg.oneshot_max_bytes)
+  if (count * dtype_size(dt) <= ll_max_bytes() && count * 8 <= c->cfg.oneshot_max_bytes)
     return run_oneshot_ll(c, local_bufs, count, dt, sig, s);
 #define HFR_ONESHOT_FN(E) (const void*)hfr_oneshot_kernel<E, 0>
   const void* fn = HFR_BY_DTYPE(dt, HFR_ONESHOT_FN);

@@ -34,6 +34,7 @@ def main():
     p.add_argument("--nccl", action="store_true")
     p.add_argument("--graph", action="store_true", help="time `iters` calls captured in one CUDA graph")
     p.add_argument("--nvls", type=int, default=0, help="NVLS arena bytes per rank (enables algo nvls)")
+    p.add_argument("--oneshot-max", type=int, default=0, help="hfr_config.oneshot_max_bytes (init-time)")
     p.add_argument("--coll", default="allreduce", choices=["allreduce", "reduce_scatter", "allgather", "reduce",
                                                              "broadcast"])
     p.add_argument("--out", default="")
@@ -58,8 +59,8 @@ def main():
     tdt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
     esz = 2 if a.dtype == "bf16" else 4
     sizes = [int(s) for s in a.sizes.split(",")]
-    comm = (hfr.Comm.init(device=local, config=hfr.Config(nvls_bytes=a.nvls)) if multi
-            else hfr.Comm.virtual_ranks(n, local))
+    comm = (hfr.Comm.init(device=local, config=hfr.Config(nvls_bytes=a.nvls, oneshot_max_bytes=a.oneshot_max))
+            if multi else hfr.Comm.virtual_ranks(n, local, hfr.Config(oneshot_max_bytes=a.oneshot_max)))
     big = max(sizes) // esz
     bufs = comm.empty(big, tdt)
     bufs = bufs if isinstance(bufs, list) else [bufs]
