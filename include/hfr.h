@@ -61,9 +61,9 @@ typedef enum {
  *            rank-ascending fold (Algorithm 1 order).
  *   ONESHOT  small messages: every rank pushes its whole buffer into every
  *            peer's inbox, then folds all n copies locally in rank order.  Same
- *            result bits as FLAT; one cross-rank handoff instead of two.  Up to
- *            64 KiB the flag travels inside each 8-byte data word (LL form, no
- *            fence: ~5 us on 4 B200s).
+ *            result bits as FLAT; one cross-rank handoff instead of two.  For
+ *            small messages the flag travels inside each 8-byte data word (LL
+ *            form, no fence: ~5 us on 4 B200s).
  *   DBT      the paper's double binary tree (Algorithm 2) as
  *            a push-only P2P schedule over the GPUs; chunk c rides tree c mod 2.
  *   PAIR_DBT "HFReduce with NVLink": pair (2k,2k+1) reduce,
@@ -82,7 +82,9 @@ typedef enum {
  *            Needs hfr_config.nvls_bytes > 0 at init and a buffer from
  *            hfr_mem_alloc inside that arena; otherwise UNSUPPORTED (never a
  *            silent change of numerics).
- *   AUTO     ONESHOT (LL form) up to 64 KiB, FLAT above (never NVLS). */
+ *   AUTO     ONESHOT (LL form) while each rank pushes <= 6 MiB of LL words
+ *            ((n-1) * count * 8 bytes: bf16 <= 256 KiB at n=4, <= 1 MiB at n=2),
+ *            FLAT above (never NVLS). */
 typedef enum {
     HFR_ALGO_AUTO = 0,
     HFR_ALGO_FLAT = 1,
@@ -111,9 +113,9 @@ typedef struct {
     float scale;          /* gradient scale, multiplies the fp32 total once (reading R3); 1.0 = sum */
     size_t scratch_bytes; /* per-rank library scratch (staging + tree partials); 0 -> 256 MiB */
     int timeout_ms;       /* cross-rank spin-wait timeout; 0 -> 60000 */
-    size_t oneshot_max_bytes; /* largest message for an explicit ONESHOT (AUTO switches at 64 KiB);
-                                 fixed at init (sizes the per-rank inbox: 2 * nranks * this);
-                                 0 -> 512 KiB */
+    size_t oneshot_max_bytes; /* ONESHOT inbox slot bytes, fixed at init (per-rank inbox =
+                                 2 * nranks * this); the largest message for an explicit ONESHOT;
+                                 the LL form needs 8 * count <= this.  0 -> 4 MiB */
     int stream_gate;      /* 1: before launching an SM schedule, make the stream wait (stream memory
                              operations in the copy-engine front end, no SM) until every rank has
                              reached this call, so no CTA spins on a late peer (overlap with compute);

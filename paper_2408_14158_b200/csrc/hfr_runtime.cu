@@ -209,14 +209,25 @@ size_t dtype_size(hfr_dtype_t t) { return t == HFR_FLOAT32 ? 4 : 2; }
 
 // An explicit ONESHOT on a message above oneshot_max_bytes runs FLAT (same
 // result bits).
-int effective_algo(const hfr_comm_s* c, size_t bytes) {
+// ONESHOT's LL form fits when every element's 8-byte word fits the inbox
+// slot; AUTO takes it while the (n-1) * count * 8 bytes each rank pushes stay
+// under ~6 MiB — the r01 graph sweep's crossover with FLAT on 2 and 4 B200s
+// (bf16: n=4 up to 256 KiB, n=2 up to 1 MiB; fp32: n=4 up to 512 KiB).
+bool ll_fits(const hfr_comm_s* c, size_t count) { return count * 8 <= c->cfg.oneshot_max_bytes; }
+bool ll_pays(const hfr_comm_s* c, size_t count) {
+  static const char* env = getenv("HFR_LL_PUSH_MAX");
+  static const uint64_t push_max = env ? strtoull(env, nullptr, 10) : (6ull << 20);
+  return (uint64_t)(c->n - 1) * count * 8 <= push_max;
+}
+
+int effective_algo(const hfr_comm_s* c, size_t count, size_t esz) {
+  const size_t bytes = count * esz;
   const int a = c->cfg.algo;
   // CE needs separate processes (stream waits across ranks) and shards of at
   // least 4096 elements; otherwise it runs FLAT (same bits)
   if (a == HFR_ALGO_CE) return (c->virt || c->n == 1 || bytes < (size_t)c->n * 16384) ? HFR_ALGO_FLAT : HFR_ALGO_CE;
-  // AUTO: ONESHOT only in its LL form (<= 64 KiB, ~5 us on 4 B200s); above
-  // that FLAT is faster than the fenced ONESHOT (r01 graph sweep)
-  if (a == HFR_ALGO_AUTO) return bytes <= std::min<size_t>(64u << 10, c->cfg.oneshot_max_bytes / 8 * 2) ? HFR_ALGO_ONESHOT : HFR_ALGO_FLAT;
+  // AUTO: ONESHOT only in its LL form and only where it beats FLAT
+  if (a == HFR_ALGO_AUTO) return ll_fits(c, count) && ll_pays(c, count) ? HFR_ALGO_ONESHOT : HFR_ALGO_FLAT;
   if (a == HFR_ALGO_ONESHOT) return bytes <= c->cfg.oneshot_max_bytes ? HFR_ALGO_ONESHOT : HFR_ALGO_FLAT;
   return a;
 }
@@ -238,7 +249,7 @@ void resolve_defaults(hfr_config_t& c) {
   if (c.chunk_elems == 0) c.chunk_elems = 32768;
   if (c.scratch_bytes == 0) c.scratch_bytes = 256ull << 20;
   if (c.timeout_ms == 0) c.timeout_ms = 60000;
-  if (c.oneshot_max_bytes == 0) c.oneshot_max_bytes = 512u << 10;
+  if (c.oneshot_max_bytes == 0) c.oneshot_max_bytes = 4u << 20;
   c.oneshot_max_bytes = round_up(c.oneshot_max_bytes, 256);
 }
 
@@ -694,12 +705,6 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   return HFR_SUCCESS;
 }
 
-// ONESHOT uses the LL (flag-in-data) form up to here (env HFR_LL_MAX for sweeps)
-uint64_t ll_max_bytes() {
-  static const uint64_t v = getenv("HFR_LL_MAX") ? strtoull(getenv("HFR_LL_MAX"), nullptr, 10) : (64u << 10);
-  return v;
-}
-
 hfr_status_t run_oneshot_ll(hfr_comm_s* c, char* const* local_bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                             cudaStream_t s) {
   const void* fn;
@@ -729,7 +734,7 @@ hfr_status_t run_oneshot_ll(hfr_comm_s* c, char* const* local_bufs, uint64_t cou
 hfr_status_t run_oneshot(hfr_comm_s* c, char* const* local_bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                          cudaStream_t s) {
   // LL form: 8 inbox bytes per element, one NVLink write of latency
-  if (count * dtype_size(dt) <= ll_max_bytes() && count * 8 <= c->cfg.oneshot_max_bytes)
+  if (ll_fits(c, count) && (c->cfg.algo == HFR_ALGO_AUTO || ll_pays(c, count)))
     return run_oneshot_ll(c, local_bufs, count, dt, sig, s);
 #define HFR_ONESHOT_FN(E) (const void*)hfr_oneshot_kernel<E, 0>
   const void* fn = HFR_BY_DTYPE(dt, HFR_ONESHOT_FN);
@@ -933,7 +938,7 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
   if (op != HFR_SUM) return HFR_ERR_UNSUPPORTED;
   if (c->sticky != HFR_SUCCESS) return c->sticky;
   // the other collectives run on the FLAT kernel's routing (NEXT-3)
-  const int algo = coll == HFR_ALLREDUCE ? effective_algo(c, count * dtype_size(dt)) : HFR_ALGO_FLAT;
+  const int algo = coll == HFR_ALLREDUCE ? effective_algo(c, count, dtype_size(dt)) : HFR_ALGO_FLAT;
   if (algo == HFR_ALGO_PAIR_DBT && c->n % 2 != 0) return HFR_ERR_UNSUPPORTED;
   if (algo == HFR_ALGO_NVLS && (c->virt || !c->nvls || !c->nvls->on)) return HFR_ERR_UNSUPPORTED;
   for (int q = 0; q < c->local; ++q)

@@ -53,7 +53,7 @@ def test_config_default():
     hfr.lib().hfr_config_default(ctypes.byref(c))
     assert c.algo == hfr.ALGO_AUTO and c.scale == 1.0
     assert c.chunk_elems == 32768 and c.threads == 0 and c.timeout_ms > 0
-    assert c.oneshot_max_bytes == 512 << 10
+    assert c.oneshot_max_bytes == 4 << 20
 
 
 def test_argument_validation_without_gpu():

@@ -287,3 +287,14 @@ def test_fuzz_configs(hfr, case):
                symmetric=c["mem"] != "plain", offset=1 if c["mem"] == "offset" else 0, async_op=c["async_op"])
     want = O.allreduce(xs, c["algo"], chunk_elems=c["chunk"], scale=c["scale"])[0]
     check(outs, want, str(c))
+
+
+@pytest.mark.parametrize("n", [2, 8])
+@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16])
+def test_oneshot_fenced_form(hfr, n, dtype):
+    """Explicit ONESHOT above the LL threshold runs the fenced push form
+    ((n-1) * count * 8 bytes > 6 MiB, message still within the inbox slot)."""
+    N = 450_001 if n == 8 else 1_000_003
+    xs = gen.rank_inputs(n, N, dtype, "normal", seed_base=91)
+    outs = run(hfr, n, xs, "oneshot", scale=0.5)
+    check(outs, O.allreduce(xs, "flat", scale=0.5)[0], f"fenced oneshot n={n}")
