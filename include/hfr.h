@@ -216,8 +216,12 @@ hfr_status_t hfr_allreduce_virtual(hfr_comm_t comm, void* const* bufs, size_t co
  *   HFR_REDUCE          root's buf := the allreduce result; other ranks' buf unchanged.
  *   HFR_BROADCAST       every rank's buf := root's buf (raw bytes).
  *   HFR_ALLREDUCE       = hfr_allreduce (every schedule of hfr_config_t.algo).
- * The non-allreduce collectives always run the FLAT kernel (bit-exact, same
- * fold order).  root is ignored except for REDUCE / BROADCAST. */
+ * The non-allreduce collectives run the FLAT kernel (bit-exact, same fold
+ * order), except with hfr_config_t.algo == HFR_ALGO_NVLS on a buffer inside
+ * the NVLS arena: then they run on the multicast object — ALLGATHER and
+ * BROADCAST by multimem.st (bit-exact), REDUCE_SCATTER and REDUCE by
+ * multimem.ld_reduce (order-relaxed, reading R18), UNSUPPORTED elsewhere.
+ * root is ignored except for REDUCE / BROADCAST. */
 typedef enum {
     HFR_ALLREDUCE = 0,
     HFR_REDUCE_SCATTER = 1,

@@ -83,6 +83,8 @@ struct Args {
   int tma_tile;            // FLAT TMA kernel: bytes per source per stage (multiple of 16)
   int tree_interleave;     // tree kernels: interleave down passes with up passes
   int excl_root;           // FLAT kernel: >= 0: this rank owns no shard (reduce/broadcast root)
+  int nvls_op;             // NVLS kernel: bit0 multimem.ld_reduce (else local load), bit1 multimem.st (else local store)
+  int nvls_solo;           // NVLS kernel: >= 0: this rank alone covers the whole buffer (reduce/broadcast root)
   char* mcbuf;              // NVLS: multicast VA of this call's buffer
   uint32_t* mc_exit;       // NVLS: multicast VA of the exit counters [kMaxCtas]
   uint32_t* uc_exit;       // NVLS: local unicast VA of the same counters
@@ -941,6 +943,115 @@ __device__ __forceinline__ void nvls_vecs_16(char* mc, uint64_t stride_bytes, in
                    "f"(__uint_as_float(v[u].w))
                    : "memory");
     }
+}
+
+// The other collectives on the multicast object (bit-exact where nothing is
+// reduced): RED loads through multimem.ld_reduce (else a local 16-B load of
+// this rank's buffer), MC stores through multimem.st (else a local store).
+//   reduce-scatter: RED, local store   all-gather: local load, MC
+//   reduce:         RED, local store (root alone, whole buffer)
+//   broadcast:      local load, MC   (root alone, whole buffer)
+template <class E, bool RED, bool MC, int U>
+__device__ __forceinline__ void nvls_vecs_coll(char* mc, char* uc, uint64_t stride_bytes, int cnt, float scale) {
+  uint4 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (u < cnt) {
+      if constexpr (!RED) {
+        v[u] = ld128(uc + u * stride_bytes);
+      } else if constexpr (std::is_same<E, F32>::value) {
+        asm volatile("multimem.ld_reduce.weak.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                     : "l"(mc + u * stride_bytes)
+                     : "memory");
+      } else if constexpr (std::is_same<E, BF16>::value) {
+        asm volatile("multimem.ld_reduce.weak.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                     : "l"(mc + u * stride_bytes)
+                     : "memory");
+      } else {
+        asm volatile("multimem.ld_reduce.weak.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                     : "l"(mc + u * stride_bytes)
+                     : "memory");
+      }
+    }
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (u < cnt) {
+      if (RED && scale != 1.0f) {
+        float f[E::kPerVec];
+        E::widen(v[u], f);
+#pragma unroll
+        for (int k = 0; k < E::kPerVec; ++k) f[k] = __fmul_rn(f[k], scale);
+        v[u] = E::narrow(f);
+      }
+      if constexpr (MC)
+        mc_st128(mc + u * stride_bytes, v[u]);
+      else
+        st128(uc + u * stride_bytes, v[u]);
+    }
+}
+
+template <class E, bool RED, bool MC>
+__device__ __forceinline__ void nvls_coll_range(const Args& a, char* uc, uint64_t lo, uint64_t hi, Pad* mine) {
+  constexpr int U = 4;
+  const uint64_t lane = threadIdx.x & 31;
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(&mine->tile_next);
+  for (;;) {
+    uint64_t t = 0;
+    if (lane == 0) t = atomicAdd(ctr, 1ull);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    const uint64_t i = lo + t * (U * 32) + lane;
+    if (lo + t * (U * 32) >= hi) break;
+    const int cnt = i < hi ? (int)((hi - i + 31) / 32) : 0;
+    nvls_vecs_coll<E, RED, MC, U>(a.mcbuf + i * 16, uc + i * 16, 32 * 16, cnt < U ? cnt : U, a.scale);
+  }
+}
+
+template <class E>
+__global__ void __launch_bounds__(512) hfr_nvls_coll_kernel(const Args a) {
+  const int rank = a.rank0;  // real comms only
+  const int n = a.n;
+  const int b = blockIdx.x;
+  Pad* const mine = a.pad[rank];
+  const uint64_t e = begin_epoch(mine);
+  __shared__ uint32_t s_k;
+  if (threadIdx.x == 0) s_k = ++mine->nvls_seq[b];
+  if (entry_barrier(a, rank, b, e)) {
+    constexpr int K = E::kPerVec;
+    const uint64_t nvec = a.count / K;
+    const bool solo = a.nvls_solo >= 0;
+    if (!solo || rank == a.nvls_solo) {
+      const uint64_t lo = solo ? 0 : nvec * rank / n, hi = solo ? nvec : nvec * (rank + 1) / n;
+      char* uc = a.buf[rank];
+      switch (a.nvls_op) {
+        case 1: nvls_coll_range<E, true, false>(a, uc, lo, hi, mine); break;
+        case 2: nvls_coll_range<E, false, true>(a, uc, lo, hi, mine); break;
+        default: nvls_coll_range<E, true, true>(a, uc, lo, hi, mine); break;
+      }
+      // ragged tail (< K elements): the last worker, over unicast peers
+      const uint64_t t0 = nvec * K;
+      if ((solo || rank == n - 1) && b == 0 && threadIdx.x < a.count - t0) {
+        const uint64_t el = t0 + threadIdx.x;
+        float acc;
+        if (a.nvls_op & 1) {
+          acc = E::load1(a.buf[0], el);
+          for (int r = 1; r < n; ++r) acc = __fadd_rn(acc, E::load1(a.buf[r], el));
+          acc = __fmul_rn(acc, a.scale);
+        } else {
+          acc = E::load1(a.buf[rank], el);
+        }
+        if (a.nvls_op & 2) {
+          for (int r = 0; r < n; ++r) E::store1(a.buf[r], el, acc);
+        } else {  // reduce root, or reduce-scatter's last shard (this rank)
+          E::store1(a.buf[rank], el, acc);
+        }
+      }
+    }
+    mc_exit_barrier(a, b, n, s_k);
+  }
+  end_epoch(mine, e);
 }
 
 template <class E>

@@ -554,6 +554,8 @@ void base_args(hfr_comm_s* c, Args& a, uint64_t count, uint64_t sig) {
   a.src_rank = -1;  // fold all ranks ...
   a.dst_mask = c->n >= 32 ? ~0u : ((1u << c->n) - 1);  // ... into every rank (allreduce)
   a.excl_root = -1;
+  a.nvls_op = 3;     // NVLS: ld_reduce + multicast store (allreduce)
+  a.nvls_solo = -1;
 }
 
 // FLAT-kernel routing of a collective (NEXT-3, "general reduce
@@ -872,12 +874,15 @@ hfr_status_t run_ce(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_
 }
 
 hfr_status_t run_nvls(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig, uint64_t offset,
-                      cudaStream_t s) {
+                      cudaStream_t s, int coll = HFR_ALLREDUCE, int root = 0) {
 #define HFR_NVLS_FN(E) (const void*)hfr_nvls_kernel<E>
-  const void* fn = HFR_BY_DTYPE(dt, HFR_NVLS_FN);
+#define HFR_NVLS_COLL_FN(E) (const void*)hfr_nvls_coll_kernel<E>
+  const void* fn = coll == HFR_ALLREDUCE ? HFR_BY_DTYPE(dt, HFR_NVLS_FN) : HFR_BY_DTYPE(dt, HFR_NVLS_COLL_FN);
   const int threads = cta_threads(c, 512);
   const uint64_t per = dt == HFR_FLOAT32 ? 4 : 8;
-  const uint64_t vec_per_rank = count / per / c->n + 1;
+  // reduce / broadcast: the root alone moves the whole buffer
+  const bool solo = coll == HFR_REDUCE || coll == HFR_BROADCAST;
+  const uint64_t vec_per_rank = count / per / (solo ? 1 : c->n) + 1;
   int g = 0;
   HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>((vec_per_rank + threads - 1) / threads, kMaxCtas), &g));
   Args a;
@@ -886,6 +891,13 @@ hfr_status_t run_nvls(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   a.mcbuf = (char*)c->nvls->mcva + offset;
   a.mc_exit = (uint32_t*)c->nvls->mcva;
   a.uc_exit = (uint32_t*)c->nvls->uc[c->rank];
+  switch (coll) {
+    case HFR_REDUCE_SCATTER: a.nvls_op = 1; break;
+    case HFR_ALLGATHER: a.nvls_op = 2; break;
+    case HFR_REDUCE: a.nvls_op = 1; a.nvls_solo = root; break;
+    case HFR_BROADCAST: a.nvls_op = 2; a.nvls_solo = root; break;
+    default: a.nvls_op = 3;
+  }
   return launch(c, fn, g, threads, a, s);
 }
 
@@ -938,7 +950,10 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
   if (op != HFR_SUM) return HFR_ERR_UNSUPPORTED;
   if (c->sticky != HFR_SUCCESS) return c->sticky;
   // the other collectives run on the FLAT kernel's routing (NEXT-3)
-  const int algo = coll == HFR_ALLREDUCE ? effective_algo(c, count, dtype_size(dt)) : HFR_ALGO_FLAT;
+  // (algo NVLS: every collective on the multicast object)
+  const int algo = coll == HFR_ALLREDUCE ? effective_algo(c, count, dtype_size(dt))
+                   : c->cfg.algo == HFR_ALGO_NVLS ? HFR_ALGO_NVLS
+                                                  : HFR_ALGO_FLAT;
   if (algo == HFR_ALGO_PAIR_DBT && c->n % 2 != 0) return HFR_ERR_UNSUPPORTED;
   if (algo == HFR_ALGO_NVLS && (c->virt || !c->nvls || !c->nvls->on)) return HFR_ERR_UNSUPPORTED;
   for (int q = 0; q < c->local; ++q)
@@ -1007,7 +1022,7 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     sig = fnv(sig, offset);
     if (algo == HFR_ALGO_NVLS) {
       if (!zero_copy || !reg || !reg->nvls || !c->nvls || !c->nvls->on) return HFR_ERR_UNSUPPORTED;
-      HFR_TRY(run_nvls(c, bufs, count, dt, sig, offset, s));
+      HFR_TRY(run_nvls(c, bufs, count, dt, sig, offset, s, coll, root));
     } else if (algo == HFR_ALGO_CE && zero_copy) {
       HFR_TRY(run_ce(c, bufs, count, dt, s));
     } else if (algo == HFR_ALGO_FLAT || algo == HFR_ALGO_CE) {

@@ -169,6 +169,40 @@ def gpu_cases(rank, world, port, outdir):
                         res["ok"].append(name)
                     except AssertionError as e:
                         res["fail"].append(str(e)[:500])
+        # the other collectives on the multicast object: all-gather and
+        # broadcast move raw bits (bit-exact); reduce-scatter and reduce are
+        # order-relaxed on their reduced region (R18) and bit-exact elsewhere
+        if "nvls-unsupported" not in res["ok"]:
+            for dtype in (gen.FP32, gen.BF16):
+                for N in (4096 + 13, 1_000_003):
+                    xs = gen.rank_inputs(world, N, dtype, "normal", seed_base=6100 + N)
+                    t = comm.empty(N, torch_dtype(dtype))
+                    for kind in ("reduce_scatter", "allgather", "reduce", "broadcast"):
+                        for root in ((0, world - 1) if kind in ("reduce", "broadcast") else (0,)):
+                            t.copy_(to_torch(xs[rank], t.device))
+                            comm.collective(kind, t, root=root)
+                            torch.cuda.synchronize()
+                            got = to_numpy(t)
+                            name = f"nvls-{kind}/{dtype}/{N}/root{root}"
+                            try:
+                                if kind == "allgather":
+                                    assert_bit_exact(got, O.all_gather(xs)[rank], name)
+                                elif kind == "broadcast":
+                                    assert_bit_exact(got, O.broadcast(xs, root)[rank], name)
+                                else:
+                                    if kind == "reduce":
+                                        lo, hi = (0, N) if rank == root else (0, 0)
+                                    else:
+                                        lo, hi = O.shard_bounds(N, world, 4 if dtype == gen.FP32 else 8)[rank]
+                                    want = O.fold_ascending(xs, 0.5)
+                                    keep = np.ones(N, bool)
+                                    keep[lo:hi] = False
+                                    assert_bit_exact(got[keep], xs[rank][keep], name + "/untouched")
+                                    if hi > lo:
+                                        assert_within_r18(got[lo:hi], [x[lo:hi] for x in xs], want[lo:hi], 0.5, name)
+                                res["ok"].append(name)
+                            except AssertionError as e:
+                                res["fail"].append(str(e)[:500])
         # every other schedule also runs zero-copy on NVLS arena memory
         comm.set_config(hfr.Config(algo="flat", scale=0.5))
         xs = gen.rank_inputs(world, 100_000, gen.FP32, "normal", seed_base=77)

@@ -104,30 +104,51 @@ int main(int argc, char** argv) {
     CK(cudaEventCreate(&e1[g]));
   }
   const char* names[] = {"read  (pull from peers)", "write (push to peers)", "mixed (pull half, push half)",
-                         "read  one-way (GPU0 only)", "write one-way (GPU0 only)"};
-  for (int mode = 0; mode < 5; ++mode) {
+                         "read  one-way (GPU0 only)", "write one-way (GPU0 only)",
+                         "fan-in read (peers read GPU0)", "fan-in write (peers write GPU0)",
+                         "reduce pattern (root GPU0)", "root read+write only (GPU0)",
+                         "owner reads + push to root", "root pushes + owner reads"};
+  // modes 5-7 run on GPUs 1..n-1 only and load GPU0's port: 5/6 every peer
+  // reads/writes `bytes` at GPU0; 7 is the reduce collective's traffic —
+  // every non-root GPU reads a segment from each other GPU (root included)
+  // and writes one segment to the root.  GB/s is GPU0's egress (5, 7) or
+  // ingress (6, 7).  8-10 split mode 7: 8 = peers read GPU0 and write GPU0
+  // (no peer-peer reads); 9 = peers read each other (not GPU0) and write GPU0;
+  // 10 = 9 plus GPU0 pushing a segment to every peer.
+  for (int mode = 0; mode < 11; ++mode) {
     if (fence_kib && mode != 1) continue;
     for (int rep = 0; rep < 3; ++rep) {
       for (int g = 0; g < n; ++g) {
-        if (mode >= 3 && g != 0) continue;
+        if ((mode == 3 || mode == 4) && g != 0) continue;
+        if (mode >= 5 && mode != 10 && g == 0) continue;
         CK(cudaSetDevice(g));
         Ptrs p{};
         p.n = 0;
         p.flag = flags[(g + 1) % n];
         uint64_t per = nvec;
         for (int h = 0; h < n; ++h) {
-          if (h == g) continue;
+          if (h == g || ((mode == 5 || mode == 6 || mode == 8) && h != 0)) continue;
+          if ((mode == 9 || mode == 10) && h == 0) continue;
+          if (mode == 10 && g == 0) {  // the root pushes its segment to peer h
+            p.src[p.n] = local[0] + (size_t)h * nvec;
+            p.dst[p.n++] = inbox[h] + (size_t)0 * nvec;
+            continue;
+          }
           uint4* peer_slot = inbox[h] + (size_t)g * nvec;
           uint4* my_slot = local[g] + (size_t)h * nvec;
-          if (mode == 0 || mode == 3) {
+          if (mode == 0 || mode == 3 || mode == 5 || mode == 7 || mode == 8 || mode == 9 || mode == 10) {
             p.src[p.n] = peer_slot; p.dst[p.n++] = my_slot;
-          } else if (mode == 1 || mode == 4) {
+          } else if (mode == 1 || mode == 4 || mode == 6) {
             p.src[p.n] = my_slot; p.dst[p.n++] = peer_slot;
           } else {
             per = nvec / 2;
             p.src[p.n] = peer_slot; p.dst[p.n++] = my_slot;
             p.src[p.n] = my_slot + per; p.dst[p.n++] = peer_slot + per;
           }
+        }
+        if (mode >= 7 && g != 0) {  // + the owner's result segment, pushed to the root
+          p.src[p.n] = local[g] + (size_t)g * nvec;
+          p.dst[p.n++] = inbox[0] + (size_t)g * nvec;
         }
         CK(cudaEventRecord(e0[g], st[g]));
         if (fence_kib)
@@ -139,7 +160,8 @@ int main(int argc, char** argv) {
       }
       float worst = 0;
       for (int g = 0; g < n; ++g) {
-        if (mode >= 3 && g != 0) continue;
+        if ((mode == 3 || mode == 4) && g != 0) continue;
+        if (mode >= 5 && mode != 10 && g == 0) continue;
         CK(cudaSetDevice(g));
         CK(cudaEventSynchronize(e1[g]));
         float ms = 0;
