@@ -170,6 +170,41 @@ def test_bf16_exhaustive_n2_sample(hfr):
     check(outs, want, "bf16 n=2")
 
 
+def test_bf16_exhaustive_n2_all_pairs(hfr):
+    """SURVEY §8(c) "bf16 exhaustive": at n=2 EVERY (a, b) pair of bf16 bit
+    patterns (2^32 pairs, incl. NaN/Inf/subnormals/signed zeros) through the
+    FLAT kernel bench.py times, against the C oracle's rank-ascending fold,
+    in 16 slices of 2^28 pairs (512 MiB per rank each).  NaN payloads are
+    not compared (reading R5)."""
+    from oracle import cfold
+    comm = comm_for(hfr, 2)
+    comm.set_config(hfr.Config(algo="flat"))
+    M = 1 << 28
+    bufs = comm.empty(M, torch.bfloat16)
+
+    def isnan16(u):
+        return ((u & 0x7F80) == 0x7F80) & ((u & 0x7F) != 0)
+
+    idx = np.arange(M, dtype=np.uint32)
+    for sl in range(16):
+        i = idx + np.uint32(sl * M)
+        a = (i >> np.uint32(16)).astype(np.uint16)
+        b = (i & np.uint32(0xFFFF)).astype(np.uint16)
+        for buf, x in zip(bufs, (a, b)):
+            buf.copy_(to_torch(x, "cuda:0"))
+        comm.allreduce_virtual(bufs)
+        torch.cuda.synchronize()
+        assert comm.status() == hfr.SUCCESS
+        want = cfold.fold_ascending([a, b])
+        for r, buf in enumerate(bufs):
+            got = to_numpy(buf)
+            ok = (got == want) | (isnan16(got) & isnan16(want))
+            bad = np.flatnonzero(~ok)
+            assert bad.size == 0, (f"slice {sl} rank {r}: {bad.size} pairs differ, first (a,b)="
+                                   f"{[(int(a[k]), int(b[k])) for k in bad[:4]]}")
+    comm.free_all()
+
+
 @pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("N", [2_003, 20_003])
 def test_cuda_graph_replay(hfr, algo, N):
