@@ -92,6 +92,9 @@ struct hfr_req_s {
   hfr_comm_s* comm = nullptr;
 };
 
+constexpr int kCeMaxChunks = 16;           // CE schedule: pipeline depth (chunks per shard)
+constexpr uint64_t kCeMinChunkBytes = 8ull << 20;  // ... and the smallest chunk (per-chunk stream latency ~15 us)
+
 struct hfr_comm_s {
   int rank = 0, n = 1, dev = 0, local = 1;
   bool virt = false;
@@ -114,8 +117,12 @@ struct hfr_comm_s {
   // CE schedule: helper streams (one per peer) so the copy engines run the
   // n-1 pulls concurrently, fork/join events, and the host-side CE epoch
   std::vector<cudaStream_t> helpers;
-  std::vector<cudaEvent_t> ce_events;
   cudaEvent_t ce_fork = nullptr;
+  // chunk-pipelined CE: all-gather helper streams (one
+  // per peer) and one event per (peer, chunk) of the reduce-scatter pulls
+  std::vector<cudaStream_t> ag_helpers;
+  std::vector<cudaEvent_t> ag_events;
+  std::vector<cudaEvent_t> chunk_events;
   uint64_t ce_epoch = 0;
   uint64_t* trace = nullptr;  // hfr_set_trace (diagnostic)
   uint32_t trace_cap = 0;
@@ -415,7 +422,13 @@ hfr_status_t common_init(hfr_comm_s* c) {
       HFR_CU(cudaStreamCreateWithPriority(&h, cudaStreamNonBlocking, hi));
       HFR_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
       c->helpers.push_back(h);
-      c->ce_events.push_back(ev);
+      HFR_CU(cudaStreamCreateWithPriority(&h, cudaStreamNonBlocking, hi));
+      c->ag_helpers.push_back(h);
+      c->ag_events.push_back(ev);
+      for (int i = 0; i < kCeMaxChunks; ++i) {
+        HFR_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        c->chunk_events.push_back(ev);
+      }
     }
     HFR_CU(cudaEventCreateWithFlags(&c->ce_fork, cudaEventDisableTiming));
   }
@@ -803,21 +816,18 @@ hfr_status_t ce_handshake(hfr_comm_s* c, cudaStream_t s, size_t field, uint64_t 
   return HFR_SUCCESS;
 }
 
-// n-1 concurrent peer copies dst_q <- src_q (q != rank), one per helper stream
-hfr_status_t ce_pull(hfr_comm_s* c, cudaStream_t s, char* const* dst, char* const* src, const size_t* bytes) {
-  HFR_CU(cudaEventRecord(c->ce_fork, s));
-  int j = 0;
-  for (int q = 0; q < c->n; ++q) {
-    if (q == c->rank) continue;
-    HFR_CU(cudaStreamWaitEvent(c->helpers[j], c->ce_fork, 0));
-    if (bytes[q]) HFR_CU(cudaMemcpyAsync(dst[q], src[q], bytes[q], cudaMemcpyDeviceToDevice, c->helpers[j]));
-    HFR_CU(cudaEventRecord(c->ce_events[j], c->helpers[j]));
-    HFR_CU(cudaStreamWaitEvent(s, c->ce_events[j], 0));
-    ++j;
-  }
-  return HFR_SUCCESS;
-}
-
+// CE schedule, chunk-pipelined (Alg. 1's "split Dg by Chunk_Size" + the
+// paper's pipelining): shard r is cut into K chunks
+// (K the same on every rank: a function of count and n only).
+//   reduce-scatter pulls: helper stream j copies chunk i of shard r from peer
+//     q into staging slot q, back to back for i = 0..K-1 (copy engines);
+//   fold: stream s folds chunk i (SMs, local, rank order) as soon as its n-1
+//     pulls landed, then publishes ce_done[r] = (e << 20) | (i + 1) at every
+//     peer with a fenced stream write;
+//   all-gather pulls: helper stream j' waits (stream memop) until peer q
+//     published chunk i of shard q and copies it into this rank's buffer.
+// So chunk i's all-gather overlaps chunk i+1's reduce-scatter pull and fold.
+// Entry/exit: ce_ready / ce_exit handshakes (no SM involved).
 hfr_status_t run_ce(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, cudaStream_t s) {
   const int n = c->n, r = c->rank;
   const size_t esz = dtype_size(dt);
@@ -827,49 +837,95 @@ hfr_status_t run_ce(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_
   const size_t slot = round_up((count / n + 256) * esz, kAlign);
   char* stage = stage_base(c, r);
   const uint64_t e = ++c->ce_epoch;
+  StreamValueFn wr = nullptr, wt = nullptr;
+  HFR_TRY(stream_value_fns(&wr, &wt));
+  // pipeline depth: every chunk >= kCeMinChunkBytes, at most kCeMaxChunks
+  const uint64_t shard_bytes = count / n * esz;
+  const int K = (int)std::max<uint64_t>(1, std::min<uint64_t>(kCeMaxChunks, shard_bytes / kCeMinChunkBytes));
+  auto chunk = [&](int g, int i, uint64_t* b, uint64_t* len) {  // chunk i of shard g, elements
+    const uint64_t L = lo[g + 1] - lo[g];
+    const uint64_t C = (L + K - 1) / K / 256 * 256 + 256;
+    const uint64_t s0 = std::min<uint64_t>(L, (uint64_t)i * C), s1 = std::min<uint64_t>(L, (uint64_t)(i + 1) * C);
+    *b = lo[g] + s0;
+    *len = (i == K - 1 ? L : s1) - s0;
+  };
   // 1. every rank's buffer is ready ("wait for chunk-i transfer")
   HFR_TRY(ce_handshake(c, s, offsetof(Pad, ce_ready), e));
-  // 2. reduce-scatter, transfer half: pull shard r of every peer (copy engines)
-  char* dst[kMaxRanks];
-  char* src[kMaxRanks];
-  size_t len[kMaxRanks];
+  HFR_CU(cudaEventRecord(c->ce_fork, s));
+  // 2. reduce-scatter transfers: all chunks, back to back, per peer
+  int j = 0;
   for (int q = 0; q < n; ++q) {
-    dst[q] = stage + (size_t)q * slot;
-    src[q] = bufs[q] + lo[r] * esz;
-    len[q] = q == r ? 0 : (lo[r + 1] - lo[r]) * esz;
+    if (q == r) continue;
+    HFR_CU(cudaStreamWaitEvent(c->helpers[j], c->ce_fork, 0));
+    for (int i = 0; i < K; ++i) {
+      uint64_t b, len;
+      chunk(r, i, &b, &len);
+      if (len)
+        HFR_CU(cudaMemcpyAsync(stage + (size_t)q * slot + (b - lo[r]) * esz, bufs[q] + b * esz, len * esz,
+                               cudaMemcpyDeviceToDevice, c->helpers[j]));
+      HFR_CU(cudaEventRecord(c->chunk_events[(size_t)j * kCeMaxChunks + i], c->helpers[j]));
+    }
+    ++j;
   }
-  HFR_TRY(ce_pull(c, s, dst, src, len));
-  // 3. reduce-scatter, arithmetic half: rank-ordered fold of shard r (SMs, local)
-  FoldArgs f{};
-  for (int q = 0; q < n; ++q) f.src[q] = q == r ? bufs[r] + lo[r] * esz : dst[q];
-  f.dst = bufs[r] + lo[r] * esz;
-  f.count = lo[r + 1] - lo[r];
-  f.scale = c->cfg.scale;
-  f.n = n;
-  const int ctas = (int)std::max<uint64_t>(1, std::min<uint64_t>(c->cfg.max_ctas > 0 ? c->cfg.max_ctas : c->num_sms,
-                                                                  (f.count / 4 + 511) / 512));
-  if (dt == HFR_BFLOAT16)
-    hfr_local_fold_kernel<BF16><<<ctas, 512, 0, s>>>(f);
-  else if (dt == HFR_FLOAT16)
-    hfr_local_fold_kernel<F16><<<ctas, 512, 0, s>>>(f);
-  else
-    hfr_local_fold_kernel<F32><<<ctas, 512, 0, s>>>(f);
-  cudaError_t err = cudaGetLastError();
-  if (err != cudaSuccess) {
-    note_cuda(err, "hfr_local_fold_kernel");
-    return HFR_ERR_CUDA;
+  for (int jj = 0; jj < n - 1; ++jj) HFR_CU(cudaStreamWaitEvent(c->ag_helpers[jj], c->ce_fork, 0));
+  // 3./4. per chunk: fold (SMs, local, rank order) once its pulls landed and
+  // publish it; then the all-gather pulls of chunk i, each gated on the
+  // owner's flag.  Host submission order matters: streams may share a
+  // hardware queue, so a blocking stream wait is only ever submitted AFTER
+  // everything any rank's flag depends on (the RS pulls, this chunk's fold
+  // and flag write) — no false dependency can then deadlock the ranks.
+  for (int i = 0; i < K; ++i) {
+    for (int jj = 0; jj < n - 1; ++jj) HFR_CU(cudaStreamWaitEvent(s, c->chunk_events[(size_t)jj * kCeMaxChunks + i], 0));
+    uint64_t b, len;
+    chunk(r, i, &b, &len);
+    if (len) {
+      FoldArgs f{};
+      for (int q = 0; q < n; ++q)
+        f.src[q] = q == r ? bufs[r] + b * esz : stage + (size_t)q * slot + (b - lo[r]) * esz;
+      f.dst = bufs[r] + b * esz;
+      f.count = len;
+      f.scale = c->cfg.scale;
+      f.n = n;
+      const int ctas = (int)std::max<uint64_t>(
+          1, std::min<uint64_t>(c->cfg.max_ctas > 0 ? c->cfg.max_ctas : c->num_sms, (len / 4 + 511) / 512));
+      if (dt == HFR_BFLOAT16)
+        hfr_local_fold_kernel<BF16><<<ctas, 512, 0, s>>>(f);
+      else if (dt == HFR_FLOAT16)
+        hfr_local_fold_kernel<F16><<<ctas, 512, 0, s>>>(f);
+      else
+        hfr_local_fold_kernel<F32><<<ctas, 512, 0, s>>>(f);
+      cudaError_t err = cudaGetLastError();
+      if (err != cudaSuccess) {
+        note_cuda(err, "hfr_local_fold_kernel");
+        return HFR_ERR_CUDA;
+      }
+      ++c->launches;
+    }
+    for (int q = 0; q < n; ++q) {
+      if (q == r) continue;
+      const unsigned long long dst = (unsigned long long)(c->pad.base[q] + offsetof(Pad, ce_done) + 8 * (size_t)r);
+      if (wr(s, dst, (e << 20) | (uint64_t)(i + 1), kWriteFenced) != 0) {
+        g_cuda_error = "cuStreamWriteValue64 on peer memory failed";
+        return HFR_ERR_CUDA;
+      }
+    }
+    int jq = 0;
+    for (int q = 0; q < n; ++q) {
+      if (q == r) continue;
+      cudaStream_t h = c->ag_helpers[jq++];
+      const unsigned long long flag = (unsigned long long)(c->pad.base[r] + offsetof(Pad, ce_done) + 8 * (size_t)q);
+      if (wt(h, flag, (e << 20) | (uint64_t)(i + 1), kWaitGeq) != 0) {
+        g_cuda_error = "cuStreamWaitValue64 failed";
+        return HFR_ERR_CUDA;
+      }
+      uint64_t qb, qlen;
+      chunk(q, i, &qb, &qlen);
+      if (qlen) HFR_CU(cudaMemcpyAsync(bufs[r] + qb * esz, bufs[q] + qb * esz, qlen * esz, cudaMemcpyDeviceToDevice, h));
+    }
   }
-  ++c->launches;
-  // 4. every owner's result shard is final
-  HFR_TRY(ce_handshake(c, s, offsetof(Pad, ce_done), e));
-  // 5. all-gather: pull every peer's result shard into my buffer (copy engines)
-  for (int q = 0; q < n; ++q) {
-    dst[q] = bufs[r] + lo[q] * esz;
-    src[q] = bufs[q] + lo[q] * esz;
-    len[q] = q == r ? 0 : (lo[q + 1] - lo[q]) * esz;
-  }
-  HFR_TRY(ce_pull(c, s, dst, src, len));
-  // 6. every rank finished pulling from every buffer
+  for (int jj = 0; jj < n - 1; ++jj) HFR_CU(cudaEventRecord(c->ag_events[jj], c->ag_helpers[jj]));
+  for (int jj = 0; jj < n - 1; ++jj) HFR_CU(cudaStreamWaitEvent(s, c->ag_events[jj], 0));
+  // 5. every rank finished pulling from every buffer
   return ce_handshake(c, s, offsetof(Pad, ce_exit), e);
 }
 
@@ -1288,7 +1344,9 @@ hfr_status_t hfr_finalize(hfr_comm_t c) {
     }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     for (cudaStream_t h : c->helpers) cudaStreamDestroy(h);
-    for (cudaEvent_t e : c->ce_events) cudaEventDestroy(e);
+    for (cudaStream_t h : c->ag_helpers) cudaStreamDestroy(h);
+    for (cudaEvent_t e : c->ag_events) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->chunk_events) cudaEventDestroy(e);
     if (c->ce_fork) cudaEventDestroy(c->ce_fork);
     if (c->side_tail) cudaEventDestroy(c->side_tail);
     if (c->side) cudaStreamDestroy(c->side);
