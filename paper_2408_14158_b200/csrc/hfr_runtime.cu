@@ -253,7 +253,7 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
 }
 
 void resolve_defaults(hfr_config_t& c) {
-  if (c.chunk_elems == 0) c.chunk_elems = 32768;
+  // chunk_elems stays 0 = "per n" (tree_chunk)
   if (c.scratch_bytes == 0) c.scratch_bytes = 256ull << 20;
   if (c.timeout_ms == 0) c.timeout_ms = 60000;
   if (c.oneshot_max_bytes == 0) c.oneshot_max_bytes = 4u << 20;
@@ -456,6 +456,14 @@ hfr_status_t common_init(hfr_comm_s* c) {
 // the message][tree partials].  Depends only on (count, dtype, algo) so every
 // rank grows in lockstep.
 size_t inbox_bytes(const hfr_comm_s* c) { return round_up(2 * (size_t)c->n * c->cfg.oneshot_max_bytes, kAlign); }
+
+// tree chunk (Alg. 1 "Chunk_Size"): the configured one, else per n — r01
+// sweeps (C2 fp32): n=2 best at 16384 (572-590 vs 520 GB/s at 32768),
+// n>=4 at 24576-32768
+uint64_t tree_chunk(const hfr_comm_s* c) {
+  if (c->cfg.chunk_elems) return c->cfg.chunk_elems;
+  return c->n == 2 ? 16384 : 32768;
+}
 
 size_t scratch_need(const hfr_comm_s* c, size_t count, hfr_dtype_t dt, int algo) {
   size_t stage = round_up(count * dtype_size(dt), kAlign);
@@ -676,7 +684,7 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   // 2 CTAs x 256 threads per SM: while one CTA drains its chunk's stores at
   // the per-chunk system fence the other issues (r01: DBT n=4 377 -> 422 GB/s)
   const int threads = cta_threads(c, 256);
-  const uint64_t C = c->cfg.chunk_elems;
+  const uint64_t C = tree_chunk(c);
   Args a;
   base_args(c, a, count, 0);
   const size_t stage = round_up(count * dtype_size(dt), kAlign);
@@ -1074,7 +1082,7 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
       }
     }
     sig = fnv(sig, (uint64_t)zero_copy);
-    sig = fnv(sig, algo == HFR_ALGO_FLAT ? 0 : c->cfg.chunk_elems);
+    sig = fnv(sig, algo == HFR_ALGO_FLAT ? 0 : tree_chunk(c));
     sig = fnv(sig, offset);
     if (algo == HFR_ALGO_NVLS) {
       if (!zero_copy || !reg || !reg->nvls || !c->nvls || !c->nvls->on) return HFR_ERR_UNSUPPORTED;

@@ -52,7 +52,7 @@ def test_config_default():
     c = hfr._Config()
     hfr.lib().hfr_config_default(ctypes.byref(c))
     assert c.algo == hfr.ALGO_AUTO and c.scale == 1.0
-    assert c.chunk_elems == 32768 and c.threads == 0 and c.timeout_ms > 0
+    assert c.chunk_elems == 0 and c.threads == 0 and c.timeout_ms > 0
     assert c.oneshot_max_bytes == 4 << 20
 
 
