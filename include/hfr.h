@@ -176,6 +176,13 @@ hfr_status_t hfr_mem_free(hfr_comm_t comm, void* ptr);
  * Idempotent per allocation.  Real comms only (virtual comms: no-op). */
 hfr_status_t hfr_register(hfr_comm_t comm, void* ptr, size_t bytes);
 
+/* COLLECTIVE.  Undo hfr_register for the registered allocation containing
+ * `ptr` (drains this device, then every peer closes its IPC mapping).  Call
+ * before freeing registered memory: a later allocation at the same address
+ * must not reuse stale peer mappings.  INVALID_ARGUMENT if `ptr` lies in no
+ * registered range; virtual comms: no-op. */
+hfr_status_t hfr_deregister(hfr_comm_t comm, void* ptr);
+
 /* COLLECTIVE, asynchronous.  In-place sum-allreduce of `count` elements of
  * `dtype` at device pointer `buf` ("Dg: data need to allreduce",
  * :367 "Dg_i is allreduced").

@@ -38,7 +38,7 @@ COLLS = {"allreduce": ALLREDUCE, "reduce_scatter": REDUCE_SCATTER, "allgather": 
 EXPORTS = (
     "hfr_config_default", "hfr_init", "hfr_init_virtual", "hfr_comm_set_config",
     "hfr_comm_local_ranks", "hfr_comm_rank", "hfr_comm_nranks", "hfr_mem_alloc", "hfr_mem_free",
-    "hfr_register", "hfr_allreduce", "hfr_allreduce_virtual", "hfr_wait", "hfr_comm_status",
+    "hfr_register", "hfr_deregister", "hfr_allreduce", "hfr_allreduce_virtual", "hfr_wait", "hfr_comm_status",
     "hfr_barrier", "hfr_finalize", "hfr_tree_query", "hfr_comm_launches", "hfr_status_string",
     "hfr_last_cuda_error", "hfr_set_trace", "hfr_collective", "hfr_collective_virtual", "hfr_shard_range",
 )
@@ -106,6 +106,7 @@ def _lib():
             "hfr_mem_alloc": (i, [vp, sz, p(vp)]),
             "hfr_mem_free": (i, [vp, vp]),
             "hfr_register": (i, [vp, vp, sz]),
+            "hfr_deregister": (i, [vp, vp]),
             "hfr_allreduce": (i, [vp, vp, sz, i, i, vp, p(vp)]),
             "hfr_allreduce_virtual": (i, [vp, p(vp), sz, i, i, vp, p(vp)]),
             "hfr_wait": (i, [vp, vp]),
@@ -317,6 +318,10 @@ class Comm:
         """Make a cudaMalloc'ed tensor peer visible (COLLECTIVE) for zero-copy."""
         _check(_lib().hfr_register(self._h, ctypes.c_void_p(tensor.data_ptr()),
                                    tensor.numel() * tensor.element_size()), "hfr_register")
+
+    def deregister(self, tensor):
+        """Undo register() (COLLECTIVE); call before the memory is freed."""
+        _check(_lib().hfr_deregister(self._h, ctypes.c_void_p(tensor.data_ptr())), "hfr_deregister")
 
     # -- collectives ---------------------------------------------------------
     def allreduce(self, tensor, async_op: bool = False, stream=None) -> Optional[Work]:

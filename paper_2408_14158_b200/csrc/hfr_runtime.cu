@@ -1250,6 +1250,29 @@ hfr_status_t hfr_register(hfr_comm_t c, void* ptr, size_t bytes) {
   return HFR_SUCCESS;
 }
 
+hfr_status_t hfr_deregister(hfr_comm_t c, void* ptr) {
+  if (!c) return HFR_ERR_NOT_INITIALIZED;
+  if (!ptr) return HFR_ERR_INVALID_ARGUMENT;
+  if (c->virt) return HFR_SUCCESS;
+  for (size_t i = 0; i < c->regions.size(); ++i) {
+    Region& r = c->regions[i];
+    const char* b = r.base[c->rank];
+    if (!r.owned && !r.nvls && b && (const char*)ptr >= b && (const char*)ptr < b + r.bytes) {
+      DeviceGuard guard(c->dev);
+      HFR_CU(cudaDeviceSynchronize());
+      if (c->n > 1) {
+        int dummy = 0;
+        std::vector<int> all(c->n);
+        HFR_TRY(exchange(c, &dummy, all.data(), sizeof(int)));  // every rank stopped using it
+      }
+      close_region(c, r);
+      c->regions.erase(c->regions.begin() + i);
+      return HFR_SUCCESS;
+    }
+  }
+  return HFR_ERR_INVALID_ARGUMENT;
+}
+
 hfr_status_t hfr_allreduce(hfr_comm_t c, void* buf, size_t count, hfr_dtype_t dtype, hfr_op_t op,
                            hfr_stream_t stream, hfr_req_t* req) {
   if (!c) return HFR_ERR_NOT_INITIALIZED;

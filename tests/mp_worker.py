@@ -60,6 +60,8 @@ def gpu_cases(rank, world, port, outdir):
                             w.wait(host=True)
                         torch.cuda.synchronize()
                         got = to_numpy(t)
+                        if mem == "registered":
+                            comm.deregister(t)
                         want = O.allreduce(xs, algo, chunk_elems=512, scale=0.5)[0]
                         name = f"{algo}/{dtype}/{N}/{mem}"
                         try:
