@@ -106,10 +106,11 @@ typedef struct {
     size_t chunk_elems;   /* tree chunk size in elements (Alg. 1 "Chunk_Size");
                              multiple of 256; 0 -> 16384 at n=2, 32768 otherwise (measured best).
                              Changes DBT/PAIR_DBT bits (reading R8), never FLAT's. */
-    int max_ctas;         /* CTAs per rank; 0 -> one per SM (two for the tree schedules).  Caps the
-                             SMs the comm uses. */
+    int max_ctas;         /* CTAs per rank; 0 -> the schedule's measured default (FLAT with TMA
+                             staging: 2 per SM, tree schedules: 3 per SM, others: 1 per SM, never
+                             more than the work needs).  Caps the SMs the comm uses. */
     int threads;          /* threads per CTA (128..512, multiple of 32); 0 -> the schedule's default
-                             (512; 256 for the tree schedules) */
+                             (256 for FLAT with TMA staging and the tree schedules, 512 otherwise) */
     float scale;          /* gradient scale, multiplies the fp32 total once (reading R3); 1.0 = sum */
     size_t scratch_bytes; /* per-rank library scratch (staging + tree partials); 0 -> 256 MiB */
     int timeout_ms;       /* cross-rank spin-wait timeout; 0 -> 60000 */

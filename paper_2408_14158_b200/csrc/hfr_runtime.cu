@@ -681,8 +681,9 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
                       cudaStream_t s) {
 #define HFR_TREE_FN(E) tree_fn<E>(pair)
   const void* fn = HFR_BY_DTYPE(dt, HFR_TREE_FN);
-  // 2 CTAs x 256 threads per SM: while one CTA drains its chunk's stores at
-  // the per-chunk system fence the other issues (r01: DBT n=4 377 -> 422 GB/s)
+  // 3 CTAs x 256 threads per SM: while one CTA drains its chunk's stores at
+  // the per-chunk system fence the others issue (r01: DBT n=4 1 -> 2 CTAs/SM
+  // 377 -> 422 GB/s, 2 -> 3 CTAs/SM 423 -> 441; 4/SM 428-434)
   const int threads = cta_threads(c, 256);
   const uint64_t C = tree_chunk(c);
   Args a;
@@ -718,7 +719,7 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
     // tree b & 1, so the two trees' dependency chains never interleave inside
     // one CTA (a rank is the root of one tree and a leaf of the other).
     int g = 0;
-    HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>(std::max<uint64_t>(here, 2), kMaxCtas), &g, 2));
+    HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>(std::max<uint64_t>(here, 2), kMaxCtas), &g, 3));
     g = std::max(2, g & ~1);
     a.c_lo = (uint32_t)lo;
     a.c_hi = (uint32_t)hi;
