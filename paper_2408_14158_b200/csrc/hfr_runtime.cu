@@ -681,11 +681,14 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
                       cudaStream_t s) {
 #define HFR_TREE_FN(E) tree_fn<E>(pair)
   const void* fn = HFR_BY_DTYPE(dt, HFR_TREE_FN);
-  // 3 CTAs x 256 threads per SM: while one CTA drains its chunk's stores at
-  // the per-chunk system fence the others issue (r01: DBT n=4 1 -> 2 CTAs/SM
-  // 377 -> 422 GB/s, 2 -> 3 CTAs/SM 423 -> 441; 4/SM 428-434)
+  // 2-3 CTAs x 256 threads per SM: while one CTA drains its chunk's stores
+  // at the per-chunk system fence the others issue (r01, n=4: DBT 1 -> 2
+  // CTAs/SM 377 -> 422 GB/s; fp32 DBT 2 -> 3 CTAs/SM 423 -> 442 and n=2
+  // 572 -> 591, but PAIR (shared-memory partner ring) 590-609 -> 561 and
+  // bf16 DBT 388 -> 377, so those keep 2)
   const int threads = cta_threads(c, 256);
   const uint64_t C = tree_chunk(c);
+  const int per_sm = !pair && dt == HFR_FLOAT32 ? 3 : 2;
   Args a;
   base_args(c, a, count, 0);
   const size_t stage = round_up(count * dtype_size(dt), kAlign);
@@ -719,7 +722,7 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
     // tree b & 1, so the two trees' dependency chains never interleave inside
     // one CTA (a rank is the root of one tree and a leaf of the other).
     int g = 0;
-    HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>(std::max<uint64_t>(here, 2), kMaxCtas), &g, 3));
+    HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>(std::max<uint64_t>(here, 2), kMaxCtas), &g, per_sm));
     g = std::max(2, g & ~1);
     a.c_lo = (uint32_t)lo;
     a.c_hi = (uint32_t)hi;
