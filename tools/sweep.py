@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import argparse
 import itertools
+import statistics
 import json
 import os
 import sys
@@ -37,6 +38,7 @@ def main():
     p.add_argument("--oneshot-max", type=int, default=0, help="hfr_config.oneshot_max_bytes (init-time)")
     p.add_argument("--coll", default="allreduce", choices=["allreduce", "reduce_scatter", "allgather", "reduce",
                                                              "broadcast"])
+    p.add_argument("--repeats", type=int, default=5, help="timed runs per point; the median of their max-over-ranks")
     p.add_argument("--out", default="")
     a = p.parse_args()
 
@@ -69,15 +71,23 @@ def main():
     stream = torch.cuda.current_stream()
     out = open(a.out, "a") if (a.out and rank == 0) else None
 
-    def mx(v):
+    def per_rank(v):
+        """every rank's value (report the max, and min/median as skew)"""
         if not multi:
-            return v
+            return [v]
         t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        allv = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allv, t)
+        return [float(x.item()) for x in allv]
+
+    skew = {}
 
     def timeit(fn, iters):
-        for _ in range(3):
+        """SURVEY §8(d) protocol: 10 warm-up calls; `repeats` timed runs of
+        `iters` calls (barrier + device barrier before each); per run the max
+        over ranks; returns the median of those maxima (skew of that run in
+        `skew`)."""
+        for _ in range(10):
             fn()
         torch.cuda.synchronize()
         run = None
@@ -92,20 +102,28 @@ def main():
             torch.cuda.synchronize()
             g.replay()  # warm
             run = g.replay
-        if multi:
-            dist.barrier()
-        comm.barrier(stream)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        if run is not None:
-            run()
-        else:
-            for _ in range(iters):
-                fn()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        return mx(e0.elapsed_time(e1) / 1e3 / iters)
+        runs = []
+        for _ in range(max(1, a.repeats)):
+            if multi:
+                dist.barrier()
+            comm.barrier(stream)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            if run is not None:
+                run()
+            else:
+                for _ in range(iters):
+                    fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            runs.append(per_rank(e0.elapsed_time(e1) / 1e3 / iters))
+        runs.sort(key=max)
+        mid = runs[len(runs) // 2]
+        skew.clear()
+        skew.update({"us_rank_min": min(mid) * 1e6, "us_rank_median": statistics.median(mid) * 1e6,
+                     "repeats": len(runs)})
+        return max(mid)
 
     def emit(d):
         if rank == 0:
@@ -141,7 +159,7 @@ def main():
                 raise SystemExit(f"hfr error {hfr.status_string(st)}")
             emit({"impl": "hfr", "coll": a.coll, "n": n, "virtual": not multi, "graph": a.graph, "dtype": a.dtype,
                   "bytes": size, "algo": algo, "chunk": chunk, "ctas": ctas, "threads": thr, "us": t * 1e6,
-                  "busbw": size / t * fac / 1e9, "algbw": size / t / 1e9})
+                  "busbw": size / t * fac / 1e9, "algbw": size / t / 1e9, **skew})
         if multi and a.nccl:
             t_ = torch.empty(cnt, dtype=tdt, device=dev).normal_()
             o_ = torch.empty(cnt // n, dtype=tdt, device=dev)
@@ -152,7 +170,7 @@ def main():
                    "broadcast": lambda: dist.broadcast(t_, 0)}[a.coll]
             tn = timeit(nfn, iters)
             emit({"impl": "nccl", "coll": a.coll, "n": n, "graph": a.graph, "dtype": a.dtype, "bytes": size,
-                  "us": tn * 1e6, "busbw": size / tn * fac / 1e9, "algbw": size / tn / 1e9,
+                  "us": tn * 1e6, "busbw": size / tn * fac / 1e9, "algbw": size / tn / 1e9, **skew,
                   "env": {k: v for k, v in os.environ.items() if k.startswith("NCCL_")}})
             del t_
     comm.finalize()
