@@ -201,7 +201,8 @@ hfr_status_t hfr_deregister(hfr_comm_t comm, void* ptr);
  *   CUDA graphs: calls may be captured (stream capture) and replayed; launch
  *   epochs live in device memory.  The first call of a given size must run
  *   uncaptured (it may grow the scratch, which is collective); a captured
- *   call that would need more scratch returns UNSUPPORTED.
+ *   call that would need more scratch returns UNSUPPORTED, and so does a
+ *   captured HFR_ALGO_CE call (its stream-memop flags carry host epochs).
  *   Errors (returned now): NOT_INITIALIZED, INVALID_ARGUMENT (buf NULL with
  *   count > 0, unknown dtype), UNSUPPORTED (op != SUM), CUDA.  count == 0 is a
  *   successful no-op.  Cross-rank errors (PROTOCOL, TIMEOUT) surface at

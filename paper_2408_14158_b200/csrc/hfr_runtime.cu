@@ -1033,6 +1033,9 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
   const bool capturing = cap != cudaStreamCaptureStatusNone;
   if (capturing && count > 0 && scratch_need(c, count, dt, algo) > c->scratch.bytes)
     return HFR_ERR_UNSUPPORTED;  // scratch growth is collective and synchronous: call once before capturing
+  // the CE schedule's stream-memop flags carry a host-side epoch, which a
+  // replayed graph would repeat (stale flags would pass): not capturable
+  if (capturing && count > 0 && algo == HFR_ALGO_CE) return HFR_ERR_UNSUPPORTED;
 
   cudaStream_t s = user;
   if (req) {
