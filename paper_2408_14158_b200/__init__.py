@@ -405,5 +405,34 @@ class Comm:
             self._h = None
 
 
+# -- module-level convenience (hfr.init(group), hfr.allreduce(t, async_op)) --
+_default: Optional[Comm] = None
+
+
+def init(group=None, device: Optional[int] = None, config: Optional[Config] = None) -> Comm:
+    """COLLECTIVE.  Create the process's default communicator over `group`
+    (torch.distributed; default group if None) and return it."""
+    global _default
+    if _default is not None:
+        raise RuntimeError("hfr.init: already initialised (call hfr.finalize() first)")
+    _default = Comm.init(group=group, device=device, config=config)
+    return _default
+
+
+def allreduce(tensor, async_op: bool = False, stream=None) -> Optional[Work]:
+    """In-place sum-allreduce of `tensor` on the default communicator."""
+    if _default is None:
+        raise RuntimeError("hfr.allreduce: call hfr.init(group) first")
+    return _default.allreduce(tensor, async_op=async_op, stream=stream)
+
+
+def finalize() -> None:
+    """COLLECTIVE.  Tear down the default communicator."""
+    global _default
+    if _default is not None:
+        _default.finalize()
+        _default = None
+
+
 __all__ = ["Comm", "Config", "Work", "HfrError", "tree_query", "shard_range", "status_string", "lib", "LIB_PATH",
-           "EXPORTS", "COLLS"]
+           "EXPORTS", "COLLS", "init", "allreduce", "finalize"]

@@ -218,6 +218,19 @@ def gpu_cases(rank, world, port, outdir):
         except AssertionError as e:
             res["fail"].append(str(e)[:500])
         comm.finalize()
+        # module-level API (hfr.init(group) / hfr.allreduce / hfr.finalize)
+        m = hfr.init(device=rank, config=hfr.Config(scale=0.5))
+        xs = gen.rank_inputs(world, 70_001, gen.BF16, "normal", seed_base=88)
+        t = m.empty(70_001, torch.bfloat16)
+        t.copy_(to_torch(xs[rank], t.device))
+        hfr.allreduce(t, async_op=True).wait()
+        torch.cuda.synchronize()
+        try:
+            assert_bit_exact(to_numpy(t), O.fold_ascending(xs, 0.5), "module-api")
+            res["ok"].append("module-api")
+        except AssertionError as e:
+            res["fail"].append(str(e)[:500])
+        hfr.finalize()
         # timeout: rank 0 calls alone
         comm = hfr.Comm.init(device=rank, config=hfr.Config(timeout_ms=1500))
         t = comm.empty(4096, torch.float32)
