@@ -25,7 +25,7 @@ memory) share SMs with the GEMM CTAs — for an overlap of 0.85-0.89; algo
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import List, Sequence, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 
 def plan_buckets(numels: Sequence[int], bucket_elems: int) -> Tuple[List[Tuple[int, int]], List[Tuple[int, int]],
@@ -61,6 +61,7 @@ def plan_buckets(numels: Sequence[int], bucket_elems: int) -> Tuple[List[Tuple[i
 class BucketStats:
     launched: int = 0
     bytes: int = 0
+    tail: int = 0   # buckets launched with tail_config
 
 
 class HaiScaleDDP:
@@ -72,9 +73,21 @@ class HaiScaleDDP:
         ddp.finish(stream)                  (stream waits for every bucket)
     """
 
-    def __init__(self, comm, numels: Sequence[int], dtype, bucket_bytes: int = 64 << 20):
+    def __init__(self, comm, numels: Sequence[int], dtype, bucket_bytes: int = 64 << 20,
+                 config=None, tail_config=None, tail_from: Optional[int] = None):
+        """`config`: the comm config for buckets that overlap the backward
+        (e.g. few small CTAs); `tail_config`: the config for the buckets
+        completed by marking parameter `tail_from` (backward order) or a later
+        one — the last gradient GEMM of the step; nothing is left to overlap
+        them with, so they may take the whole GPU.  tail_from None: the last
+        parameter.  tail_config None: `config` throughout; both None: the
+        comm's current config.  Every rank makes the same choice for the same
+        bucket (collective contract, include/hfr.h)."""
         import torch
         self.comm = comm
+        self.config = config
+        self.tail_config = tail_config
+        self.tail_from = len(numels) - 1 if tail_from is None else tail_from
         self.dtype = dtype
         esz = torch.tensor([], dtype=dtype).element_size()
         self.bucket_elems = max(1, bucket_bytes // esz)
@@ -84,6 +97,7 @@ class HaiScaleDDP:
         if isinstance(self.arena, list):
             raise ValueError("HaiScaleDDP needs a real (one rank per process) comm")
         self._pending = [len(m) for m in self.bucket_params]
+        self._active = None
         self._bucket_of_param: List[List[int]] = [[] for _ in numels]
         for k, mem in enumerate(self.bucket_params):
             for i in mem:
@@ -106,12 +120,21 @@ class HaiScaleDDP:
         self._pending = [len(m) for m in self.bucket_params]
         self._works = []
 
+    def _use(self, cfg):
+        if cfg is not None and cfg is not self._active:
+            self.comm.set_config(cfg)
+            self._active = cfg
+
     def mark_ready(self, i: int, stream=None):
         """Parameter i's gradient has been enqueued on `stream`; launch the
-        allreduce of every bucket that just became complete."""
+        allreduce of every bucket that just became complete.  Buckets
+        completed by parameter `tail_from` or later go out with `tail_config`."""
+        tail = self.tail_config is not None and i >= self.tail_from
         for k in self._bucket_of_param[i]:
             self._pending[k] -= 1
             if self._pending[k] == 0:
+                self._use(self.tail_config if tail else self.config)
+                self.stats.tail += int(tail)
                 self._launch(k, stream)
 
     def _launch(self, k: int, stream):

@@ -109,6 +109,26 @@ def gpu_cases(rank, world, port, outdir):
             res["ok"].append("ddp")
         except AssertionError as e:
             res["fail"].append(str(e)[:500])
+        # the same with few small overlap CTAs behind the stream gate and a
+        # full-width tail (buckets completed by parameter 3 onwards): the CTA
+        # count changes between launches of one comm, bits do not
+        ddp2 = HaiScaleDDP(comm, numels, torch.bfloat16, bucket_bytes=64 << 10,
+                           config=hfr.Config(algo="flat", scale=0.5, max_ctas=4, threads=128, stream_gate=1,
+                                             flat_staging=1),
+                           tail_config=hfr.Config(algo="flat", scale=0.5), tail_from=3)
+        for step in range(2):
+            for i, (s, e) in enumerate(ddp2.param_ranges):
+                ddp2.grad(i).copy_(to_torch(xs_all[rank][s:e], ddp2.arena.device))
+                ddp2.mark_ready(i, stream)
+            ddp2.finish(stream)
+            torch.cuda.synchronize()
+            try:
+                assert 0 < ddp2.stats.tail < ddp2.stats.launched, (ddp2.stats.tail, ddp2.stats.launched)
+                assert_bit_exact(to_numpy(ddp2.arena[:ddp2.total]), O.fold_ascending(xs_all, 0.5), "ddp tail")
+                res["ok"].append(f"ddp-tail-{step}")
+            except AssertionError as e:
+                res["fail"].append(str(e)[:500])
+        comm.set_config(hfr.Config(algo="flat", scale=0.5))
         # the other collectives (NEXT-3), one rank per GPU
         comm.set_config(hfr.Config(scale=0.5))
         for kind in ("reduce_scatter", "allgather", "reduce", "broadcast"):

@@ -48,3 +48,59 @@ def test_c5_bucket_count():
 def test_bad_bucket():
     with pytest.raises(ValueError):
         plan_buckets([1], 0)
+
+
+class _FakeComm:
+    """Records (config, bucket offset) per allreduce; CPU tensors only."""
+
+    def __init__(self):
+        self.cfg, self.calls = None, []
+
+    def empty(self, numel, dtype):
+        import torch
+        return torch.zeros(numel, dtype=dtype)
+
+    def set_config(self, cfg):
+        self.cfg = cfg
+
+    def allreduce(self, t, async_op=False, stream=None):
+        self.calls.append((self.cfg, t.data_ptr()))
+
+        class _W:
+            def wait(self, stream=None):
+                pass
+        return _W()
+
+
+@pytest.mark.parametrize("tail_from", [None, 2, 4])
+def test_tail_config_covers_exactly_the_late_buckets(tail_from):
+    import torch
+    from paper_2408_14158_b200.ddp import HaiScaleDDP
+    numels = [40, 17, 100, 3, 60]
+    comm = _FakeComm()
+    ddp = HaiScaleDDP(comm, numels, torch.float32, bucket_bytes=16 * 4, config="overlap", tail_config="tail",
+                      tail_from=tail_from)
+    tf = len(numels) - 1 if tail_from is None else tail_from
+    for step in range(2):
+        comm.calls = []
+        for i in range(len(numels)):
+            ddp.mark_ready(i)
+        ddp.finish()
+        assert len(comm.calls) == len(ddp.bucket_ranges)
+        esz = 4
+        for cfg, ptr in comm.calls:
+            k = (ptr - ddp.arena.data_ptr()) // esz // ddp.bucket_elems
+            last_member = max(ddp.bucket_params[k])
+            assert cfg == ("tail" if last_member >= tf else "overlap"), (k, cfg)
+    assert ddp.stats.tail == 2 * sum(1 for m in ddp.bucket_params if max(m) >= tf)
+
+
+def test_no_configs_leaves_comm_config_alone():
+    import torch
+    from paper_2408_14158_b200.ddp import HaiScaleDDP
+    comm = _FakeComm()
+    ddp = HaiScaleDDP(comm, [10, 20], torch.float32, bucket_bytes=32)
+    for i in range(2):
+        ddp.mark_ready(i)
+    ddp.finish()
+    assert all(c is None for c, _ in comm.calls) and ddp.stats.tail == 0

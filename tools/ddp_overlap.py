@@ -52,13 +52,16 @@ def main():
     ap.add_argument("--tokens", type=int, default=4096)
     ap.add_argument("--bucket-mib", type=int, default=64)
     ap.add_argument("--max-ctas", type=int, default=24)
-    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--algo", default="flat")
     ap.add_argument("--layers", type=int, default=LAYERS, help="fewer layers for a quick run")
     ap.add_argument("--gate", type=int, default=0, help="hfr_config.stream_gate")
     ap.add_argument("--threads", type=int, default=0, help="threads per comm CTA (small CTAs can share an SM "
                                                           "with a GEMM CTA)")
     ap.add_argument("--staging", type=int, default=0, help="hfr_config.flat_staging (1 = registers)")
+    ap.add_argument("--tail", type=int, default=0, help="1: buckets completed by the last gradient GEMM (embed) "
+                                                       "use a full-width config (nothing left to overlap)")
+    ap.add_argument("--tail-algo", default="flat")
     a = ap.parse_args()
 
     import torch
@@ -82,10 +85,13 @@ def main():
                   or p[0].startswith("lm_head")]
     numels = [o * i for _, o, i in params]
     nvls = (TOTAL * 2 + (256 << 20)) if a.algo == "nvls" else 0
-    comm = hfr.Comm.init(device=local, config=hfr.Config(algo=a.algo, max_ctas=a.max_ctas, scale=1.0 / world,
-                                                        stream_gate=a.gate, nvls_bytes=nvls, threads=a.threads,
-                                                        flat_staging=a.staging))
-    ddp = HaiScaleDDP(comm, numels, torch.bfloat16, bucket_bytes=a.bucket_mib << 20)
+    cfg = hfr.Config(algo=a.algo, max_ctas=a.max_ctas, scale=1.0 / world, stream_gate=a.gate, nvls_bytes=nvls,
+                     threads=a.threads, flat_staging=a.staging)
+    comm = hfr.Comm.init(device=local, config=cfg)
+    tail_cfg = hfr.Config(algo=a.tail_algo, scale=1.0 / world, stream_gate=a.gate) if a.tail else None
+    tail_from = [nm for nm, _, _ in params].index("embed")
+    ddp = HaiScaleDDP(comm, numels, torch.bfloat16, bucket_bytes=a.bucket_mib << 20, config=cfg,
+                      tail_config=tail_cfg, tail_from=tail_from)
     T = a.tokens
     g = torch.Generator(device=dev).manual_seed(3000 + rank)
     gemm = [(o, i) for _, o, i in params if o > 1 and i <= 65536]
@@ -130,13 +136,14 @@ def main():
     comm_only()
     from bench import Clocks
     res = {"bwd": [], "comm": [], "both": []}
-    clk = {}
-    for name, fn in (("bwd", lambda: backward(False)), ("comm", comm_only), ("both", lambda: backward(True))):
-        ck = Clocks(local, interval_ms=20)
-        ck.start()
-        for _ in range(a.reps):
+    # interleaved repetitions (bwd, comm, both, bwd, ...) so slow drifts of the
+    # power-capped clock hit all three alike; overlap also reported per rep
+    ck = Clocks(local, interval_ms=20)
+    ck.start()
+    for _ in range(a.reps):
+        for name, fn in (("bwd", lambda: backward(False)), ("comm", comm_only), ("both", lambda: backward(True))):
             res[name].append(timed(fn))
-        clk[name] = ck.stop()
+    clk = {"all": ck.stop()}
     if comm.status() != hfr.SUCCESS:
         raise SystemExit(hfr.status_string(comm.status()))
     tb, tc, tt = (statistics.median(res[k]) for k in ("bwd", "comm", "both"))
@@ -150,6 +157,11 @@ def main():
             "stream_gate": a.gate, "threads": a.threads, "flat_staging": a.staging, "side_priority": os.environ.get("HFR_SIDE_PRIORITY", "high"),
             "tokens": T, "T_bwd_ms": tb * 1e3, "T_comm_ms": tc * 1e3, "T_both_ms": tt * 1e3,
             "overlap": (tb + tc - tt) / tc, "bwd_slowdown": tt / tb,
+            "overlap_paired_median": statistics.median((b + c - t) / c for b, c, t in zip(res["bwd"], res["comm"],
+                                                                                            res["both"])),
+            "overlap_min": (min(res["bwd"]) + min(res["comm"]) - min(res["both"])) / min(res["comm"]),
+            "tail": a.tail, "tail_algo": a.tail_algo if a.tail else None, "tail_buckets": sum(1 for m in ddp.bucket_params if a.tail and max(m) >= tail_from),
+            "reps_order": "interleaved",
             "comm_busbw": S / tc * 2 * (n - 1) / n / 1e9, "bwd_tflops": flops / tb / 1e12,
             "clocks": clk, "reps": res}), flush=True)
     comm.finalize()
