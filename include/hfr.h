@@ -107,7 +107,7 @@ typedef struct {
                              multiple of 256; 0 -> 16384 at n=2, 32768 otherwise (measured best).
                              Changes DBT/PAIR_DBT bits (reading R8), never FLAT's. */
     int max_ctas;         /* CTAs per rank; 0 -> the schedule's measured default (FLAT with TMA
-                             staging: 2 per SM, tree schedules: 2 per SM (fp32 DBT: 3), others: 1 per SM, never
+                             staging: 1 per SM (2 with virtual ranks), tree schedules: 2 per SM (fp32 DBT: 3), others: 1 per SM, never
                              more than the work needs).  Caps the SMs the comm uses. */
     int threads;          /* threads per CTA (128..512, multiple of 32); 0 -> the schedule's default
                              (256 for FLAT with TMA staging and the tree schedules, 512 otherwise) */

@@ -599,7 +599,11 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
                           cudaStream_t s, int coll, int root, const void* fn) {
   // experiment knobs: HFR_TMA_TILE (bytes per source per stage), HFR_TMA_PER_SM
   static const int tile = getenv("HFR_TMA_TILE") ? atoi(getenv("HFR_TMA_TILE")) : kTmaTileBytes;
-  static const int per_sm = getenv("HFR_TMA_PER_SM") ? atoi(getenv("HFR_TMA_PER_SM")) : 2;
+  // CTAs per SM: 1 for a real comm (one rank per GPU) — r01 sweep, bf16 2 MiB-256 MiB and C2:
+  // +1 % (large) to +18 % (4 MiB) over 2 per SM at n=2 and n=4, half the per-CTA handshakes
+  // (profiles/r01/tma_tile_*.jsonl); 2 for virtual ranks (all n ranks' CTAs share one GPU)
+  static const int per_sm_env = getenv("HFR_TMA_PER_SM") ? atoi(getenv("HFR_TMA_PER_SM")) : 0;
+  const int per_sm = per_sm_env > 0 ? per_sm_env : (c->virt && c->local > 1 ? 2 : 1);
   const int threads = cta_threads(c, 256);
   static const bool bs = getenv("HFR_TMA_STORE") && strcmp(getenv("HFR_TMA_STORE"), "1") == 0;
   const int smem = 2 * c->n * tile + (bs ? 2 * tile : 0);
