@@ -148,13 +148,24 @@ __device__ __forceinline__ uint64_t globaltimer() {
 // launch); the last CTA of the launch to finish publishes it.  A CTA can only
 // finish after reading, so every CTA of a launch sees the same value whatever
 // the residency, and the next launch (stream order) sees the update.
+// Programmatic dependent launch (real comms, include/hfr.h): a launch may be
+// scheduled while the previous kernel on the stream is in its exit phase.
+// pdl_wait() blocks until that kernel has completed and its memory is visible
+// (a no-op for an ordinary launch), so it comes before ANY memory access;
+// pdl_trigger() lets the next launch be scheduled once every CTA of this one
+// has reached its exit handshake (implicit at completion otherwise).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t begin_epoch(Pad* mine) {
   __shared__ uint64_t s_epoch;
+  pdl_wait();
   if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile uint64_t*>(&mine->launch_epoch) + 1;
   __syncthreads();
   return s_epoch;
 }
 __device__ __forceinline__ void end_epoch(Pad* mine, uint64_t e) {
+  pdl_trigger();
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -243,6 +254,7 @@ __device__ __forceinline__ bool entry_barrier(const Args& a, int rank, int b, ui
 // a5 completion: CTA b tells CTA b of every rank that all its loads from and
 // stores to that rank are done, and waits for the same from everyone.
 __device__ __forceinline__ void exit_barrier(const Args& a, int rank, int b, uint64_t e) {
+  pdl_trigger();
   __syncthreads();
   const int q = threadIdx.x;
   if (q < a.n) {
@@ -257,6 +269,7 @@ __device__ __forceinline__ void exit_barrier(const Args& a, int rank, int b, uin
 // each CTA b bumps counter b on every GPU with ONE multimem.red.release and
 // waits until all n ranks' CTA b arrived (k = this CTA's NVLS launch count).
 __device__ __forceinline__ void mc_exit_barrier(const Args& a, int b, int n, uint32_t k) {
+  pdl_trigger();
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t target = (uint32_t)n * k;

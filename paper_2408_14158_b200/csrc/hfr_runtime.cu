@@ -522,16 +522,35 @@ const void* tree_fn(bool pair) {
   return pair ? (const void*)hfr_tree_kernel<E, true> : (const void*)hfr_tree_kernel<E, false>;
 }
 
+// Launch one protocol kernel.  Virtual comms (all ranks' CTAs on one GPU):
+// cooperative launch, so every rank's CTAs are co-resident.  Real comms:
+// programmatic dependent launch — the kernel may be scheduled while the
+// previous kernel on the stream is in its exit handshake and waits for it in
+// hardware (pdl_wait, hfr_kernels.cuh) before touching memory; hides the
+// launch gap between back-to-back collectives.  HFR_PDL=0 turns it off (A/B).
+cudaError_t launch_protocol_kernel(const hfr_comm_s* c, const void* fn, dim3 grid, dim3 block, void** params,
+                                   size_t smem, cudaStream_t s) {
+  if (c->virt && c->local > 1) return cudaLaunchCooperativeKernel(fn, grid, block, params, smem, s);
+  static const bool pdl = !(getenv("HFR_PDL") && strcmp(getenv("HFR_PDL"), "0") == 0);
+  if (!pdl) return cudaLaunchKernel(fn, grid, block, params, smem, s);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, params);
+}
+
 hfr_status_t launch(hfr_comm_s* c, const void* fn, int grid_x, int threads, Args& a, cudaStream_t s) {
   ++c->epoch;  // host mirror (stats only): kernels keep their epoch in device memory
   void* params[] = {&a};
   dim3 grid(grid_x, c->local), block(threads);
-  cudaError_t e;
-  if (c->virt && c->local > 1) {
-    e = cudaLaunchCooperativeKernel(fn, grid, block, params, 0, s);
-  } else {
-    e = cudaLaunchKernel(fn, grid, block, params, 0, s);
-  }
+  const cudaError_t e = launch_protocol_kernel(c, fn, grid, block, params, 0, s);
   if (e != cudaSuccess) {
     note_cuda(e, "launch");
     return HFR_ERR_CUDA;
@@ -630,9 +649,7 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
   coll_routing(c, coll, root, &a.src_rank, &a.dst_mask, &a.excl_root);
   ++c->epoch;
   void* params[] = {&a};
-  cudaError_t e = (c->virt && c->local > 1)
-                      ? cudaLaunchCooperativeKernel(fn, dim3(g, c->local), dim3(threads), params, smem, s)
-                      : cudaLaunchKernel(fn, dim3(g, c->local), dim3(threads), params, smem, s);
+  cudaError_t e = launch_protocol_kernel(c, fn, dim3(g, c->local), dim3(threads), params, smem, s);
   if (e != cudaSuccess) {
     note_cuda(e, "hfr_flat_tma_kernel");
     return HFR_ERR_CUDA;
