@@ -191,10 +191,10 @@ hfr_status_t hfr_deregister(hfr_comm_t comm, void* ptr);
  *   the host immediately.  If req != NULL the work runs on the comm's side
  *   stream and *req must be passed to hfr_wait exactly once; if req == NULL it
  *   runs on `stream` itself (completion is stream-ordered).  Real comms launch
- *   their kernels as programmatic dependent launches: a kernel may become
- *   resident while the previous kernel on the stream finishes, but touches no
- *   memory before that kernel has completed (griddepcontrol.wait), so the
- *   ordering above is unchanged (HFR_PDL=0: ordinary launches).
+ *   their small-message kernels as programmatic dependent launches: a kernel
+ *   may become resident while the previous kernel on the stream finishes, but
+ *   touches no memory before that kernel has completed (griddepcontrol.wait),
+ *   so the ordering above is unchanged (HFR_PDL=0: ordinary launches).
  *   Result: every rank's buf holds identical bytes: the rank-ascending fold
  *   (FLAT), the tree-order fold (DBT) or the pair-first fold (PAIR_DBT), times
  *   scale, cast to dtype.  Buffers outside hfr_mem_alloc / hfr_register memory

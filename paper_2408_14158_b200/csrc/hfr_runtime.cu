@@ -523,15 +523,20 @@ const void* tree_fn(bool pair) {
 }
 
 // Launch one protocol kernel.  Virtual comms (all ranks' CTAs on one GPU):
-// cooperative launch, so every rank's CTAs are co-resident.  Real comms:
-// programmatic dependent launch — the kernel may be scheduled while the
-// previous kernel on the stream is in its exit handshake and waits for it in
-// hardware (pdl_wait, hfr_kernels.cuh) before touching memory; hides the
-// launch gap between back-to-back collectives.  HFR_PDL=0 turns it off (A/B).
+// cooperative launch, so every rank's CTAs are co-resident.  Real comms with
+// `pdl` (the latency-bound small-message kernels: ONESHOT, LL ONESHOT,
+// barrier): programmatic dependent launch — the kernel may be scheduled while
+// the previous kernel on the stream is in its exit handshake and waits for it
+// in hardware (pdl_wait, hfr_kernels.cuh) before touching memory.  r01, n=2,
+// bf16, CUDA graph: 1 KiB 3.93 -> 3.75 us, 64 KiB 5.12 -> 4.73, 1 MiB 12.38 ->
+// 11.98; the bandwidth kernels (FLAT, FLAT-TMA) measured slower with it at
+// 2-64 MiB eager (2 MiB 17.3 -> 20.5 us), so they launch plainly
+// (profiles/r01/pdl_ab_n2.jsonl).  HFR_PDL=0: never; HFR_PDL=2: every kernel (A/B).
 cudaError_t launch_protocol_kernel(const hfr_comm_s* c, const void* fn, dim3 grid, dim3 block, void** params,
-                                   size_t smem, cudaStream_t s) {
+                                   size_t smem, cudaStream_t s, bool pdl_ok) {
   if (c->virt && c->local > 1) return cudaLaunchCooperativeKernel(fn, grid, block, params, smem, s);
-  static const bool pdl = !(getenv("HFR_PDL") && strcmp(getenv("HFR_PDL"), "0") == 0);
+  static const int mode = getenv("HFR_PDL") ? atoi(getenv("HFR_PDL")) : 1;
+  const bool pdl = mode == 2 || (mode == 1 && pdl_ok);
   if (!pdl) return cudaLaunchKernel(fn, grid, block, params, smem, s);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -546,11 +551,12 @@ cudaError_t launch_protocol_kernel(const hfr_comm_s* c, const void* fn, dim3 gri
   return cudaLaunchKernelExC(&cfg, fn, params);
 }
 
-hfr_status_t launch(hfr_comm_s* c, const void* fn, int grid_x, int threads, Args& a, cudaStream_t s) {
+hfr_status_t launch(hfr_comm_s* c, const void* fn, int grid_x, int threads, Args& a, cudaStream_t s,
+                    bool pdl_ok = false) {
   ++c->epoch;  // host mirror (stats only): kernels keep their epoch in device memory
   void* params[] = {&a};
   dim3 grid(grid_x, c->local), block(threads);
-  const cudaError_t e = launch_protocol_kernel(c, fn, grid, block, params, 0, s);
+  const cudaError_t e = launch_protocol_kernel(c, fn, grid, block, params, 0, s, pdl_ok);
   if (e != cudaSuccess) {
     note_cuda(e, "launch");
     return HFR_ERR_CUDA;
@@ -649,7 +655,7 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
   coll_routing(c, coll, root, &a.src_rank, &a.dst_mask, &a.excl_root);
   ++c->epoch;
   void* params[] = {&a};
-  cudaError_t e = launch_protocol_kernel(c, fn, dim3(g, c->local), dim3(threads), params, smem, s);
+  cudaError_t e = launch_protocol_kernel(c, fn, dim3(g, c->local), dim3(threads), params, smem, s, false);
   if (e != cudaSuccess) {
     note_cuda(e, "hfr_flat_tma_kernel");
     return HFR_ERR_CUDA;
@@ -776,7 +782,7 @@ hfr_status_t run_oneshot_ll(hfr_comm_s* c, char* const* local_bufs, uint64_t cou
   a.slot_bytes = c->cfg.oneshot_max_bytes;
   for (int q = 0; q < c->n; ++q) a.inbox[q] = c->scratch.base[q];
   for (int q = 0; q < c->local; ++q) a.buf[c->virt ? q : c->rank] = local_bufs[q];
-  return launch(c, fn, g, threads, a, s);
+  return launch(c, fn, g, threads, a, s, true);
 }
 
 hfr_status_t run_oneshot(hfr_comm_s* c, char* const* local_bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
@@ -798,7 +804,7 @@ hfr_status_t run_oneshot(hfr_comm_s* c, char* const* local_bufs, uint64_t count,
   a.slot_bytes = c->cfg.oneshot_max_bytes;
   for (int q = 0; q < c->n; ++q) a.inbox[q] = c->scratch.base[q];
   for (int q = 0; q < c->local; ++q) a.buf[c->virt ? q : c->rank] = local_bufs[q];
-  return launch(c, fn, g, threads, a, s);
+  return launch(c, fn, g, threads, a, s, true);
 }
 
 // ---------------------------------------------------------------------------
@@ -1380,7 +1386,7 @@ hfr_status_t hfr_barrier(hfr_comm_t c, hfr_stream_t stream) {
   DeviceGuard guard(c->dev);
   Args a;
   base_args(c, a, 0, 0xBA881E8ull);
-  return launch(c, (const void*)hfr_barrier_kernel, 1, 32 * ((c->n + 31) / 32), a, (cudaStream_t)stream);
+  return launch(c, (const void*)hfr_barrier_kernel, 1, 32 * ((c->n + 31) / 32), a, (cudaStream_t)stream, true);
 }
 
 hfr_status_t hfr_finalize(hfr_comm_t c) {
