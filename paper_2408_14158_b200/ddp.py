@@ -21,7 +21,7 @@ of 15 interleaved repetitions): the best bit-exact setting is FLAT with
 Config(max_ctas=32..40, threads=128, stream_gate=1, flat_staging=1) — small
 register-staged comm CTAs (no shared memory) share SMs with the GEMM CTAs —
 plus a full-width tail_config for the buckets completed by the last gradient
-GEMM, for an overlap of 0.93-0.95 (0.91 without the tail); algo "nvls"
+GEMM, for an overlap of 0.90-0.95 over runs (0.91 without the tail); algo "nvls"
 (order-relaxed) with 16 CTAs reaches 0.98-0.99.
 """
 from __future__ import annotations
