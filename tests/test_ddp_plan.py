@@ -104,3 +104,16 @@ def test_no_configs_leaves_comm_config_alone():
         ddp.mark_ready(i)
     ddp.finish()
     assert all(c is None for c, _ in comm.calls) and ddp.stats.tail == 0
+
+
+def test_c5_tail_buckets_are_the_embedding_gemm_buckets():
+    """C5 tail (tools/ddp_overlap.py --tail 1): the buckets completed by the
+    last gradient GEMM (embedding) or later — 9 of the 209, the last one ragged."""
+    import tools.ddp_overlap as d
+    params = d.llama7b_layout()
+    numels = [o * i for _, o, i in params]
+    tail_from = [nm for nm, _, _ in params].index("embed")
+    _, buckets, members = plan_buckets(numels, (64 << 20) // 2)
+    tail = [k for k, m in enumerate(members) if max(m) >= tail_from]
+    assert tail == list(range(200, 209))
+    assert params[tail_from][1] * params[tail_from][2] > 8 * (64 << 20) // 2  # embed spans > 8 buckets
