@@ -116,4 +116,4 @@ def test_c5_tail_buckets_are_the_embedding_gemm_buckets():
     _, buckets, members = plan_buckets(numels, (64 << 20) // 2)
     tail = [k for k, m in enumerate(members) if max(m) >= tail_from]
     assert tail == list(range(200, 209))
-    assert params[tail_from][1] * params[tail_from][2] > 8 * (64 << 20) // 2  # embed spans > 8 buckets
+    assert 7 * (64 << 20) // 2 < params[tail_from][1] * params[tail_from][2] < 8 * (64 << 20) // 2  # 7.8 buckets over 9
