@@ -83,9 +83,12 @@ class HaiScaleDDP:
         one — the last gradient GEMM of the step; nothing is left to overlap
         them with, so they may take the whole GPU.  tail_from None: the last
         parameter.  tail_config None: `config` throughout; both None: the
-        comm's current config.  Every rank makes the same choice for the same
-        bucket (collective contract, include/hfr.h)."""
+        comm's current config; tail_config without config: ValueError.
+        Every rank makes the same choice for the same bucket (collective
+        contract, include/hfr.h)."""
         import torch
+        if tail_config is not None and config is None:
+            raise ValueError("tail_config needs config (the comm's config is not restored otherwise)")
         self.comm = comm
         self.config = config
         self.tail_config = tail_config

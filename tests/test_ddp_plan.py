@@ -117,3 +117,10 @@ def test_c5_tail_buckets_are_the_embedding_gemm_buckets():
     tail = [k for k, m in enumerate(members) if max(m) >= tail_from]
     assert tail == list(range(200, 209))
     assert 7 * (64 << 20) // 2 < params[tail_from][1] * params[tail_from][2] < 8 * (64 << 20) // 2  # 7.8 buckets over 9
+
+
+def test_tail_config_requires_config():
+    import torch
+    from paper_2408_14158_b200.ddp import HaiScaleDDP
+    with pytest.raises(ValueError):
+        HaiScaleDDP(_FakeComm(), [10, 20], torch.float32, bucket_bytes=32, tail_config="tail")
