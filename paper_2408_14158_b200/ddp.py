@@ -124,6 +124,7 @@ class HaiScaleDDP:
     def reset(self):
         self._pending = [len(m) for m in self.bucket_params]
         self._works = []
+        self._active = None  # re-apply the configs each step (the caller may have changed the comm's)
 
     def _use(self, cfg):
         if cfg is not None and cfg is not self._active:
