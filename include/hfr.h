@@ -73,7 +73,9 @@ typedef enum {
  *            cross-rank ordering uses stream memory operations (no SM spins),
  *            and only a short local fold kernel runs on the SMs — for
  *            overlapping with compute (DDP).  Same result bits as FLAT.
- *            Needs peer-mapped buffers on a real comm; otherwise runs FLAT.
+ *            Runs on real and virtual comms alike (virtual ranks: the copy
+ *            engines copy between the ranks' buffers on one GPU); at n = 1 or
+ *            for messages under n * 16 KiB it runs FLAT (nothing to move).
  *   NVLS     ORDER-RELAXED NVLink SHARP path: the NVSwitch sums
  *            the n copies (multimem.ld_reduce) and multicasts the owner's
  *            scaled result (multimem.st).  The switch chooses the summation
@@ -130,15 +132,24 @@ typedef struct {
                              {2,4,8}, registers otherwise), 1 registers (no shared memory: small CTAs
                              can share an SM with a compute kernel, e.g. DDP overlap), 2 TMA.  Bits
                              are identical either way. */
+    size_t ll_push_max;   /* AUTO: largest (n-1) * count * 8 bytes a rank pushes in the LL ONESHOT
+                             form before FLAT takes over; 0 -> 6 MiB (the r01 crossover on 2 and 4
+                             B200s).  Part of the call signature (it picks the schedule). */
+    int pdl_off;          /* 1: launch the latency-bound kernels (ONESHOT, LL ONESHOT, barrier) of a
+                             real comm as ordinary launches; 0 (default): programmatic dependent
+                             launches (see hfr_allreduce).  Never changes results. */
 } hfr_config_t;
 
 /* Fill *cfg with the defaults above (algo AUTO, scale 1.0). */
 void hfr_config_default(hfr_config_t* cfg);
 
 /* COLLECTIVE.  Create a communicator for `rank` of `nranks` (1..HFR_MAX_RANKS)
- * processes, each driving one GPU of this box (`cuda_device`).  Allocates the
- * peer-mapped signal pad and scratch, exchanges CUDA IPC handles through
- * `allgather(ctx)`, opens the peers' mappings.  cfg may be NULL (defaults).
+ * processes, each driving one GPU of this box (`cuda_device`) — the paper's
+ * set of GPUs that "require allreduce" together (§4 Alg. 1;
+ * :323 "GPU_Count").  Allocates the peer-mapped signal pad and scratch,
+ * exchanges CUDA IPC handles through `allgather(ctx)`, opens the peers'
+ * mappings.  cfg may be NULL (defaults).  nranks = 1 needs no callback
+ * (allgather may be NULL).
  * On success *comm is owned by the caller until hfr_finalize.
  * Errors: INVALID_ARGUMENT (comm NULL, rank out of range, nranks out of range,
  * allgather NULL with nranks > 1, bad cfg), CUDA, OUT_OF_MEMORY. */
@@ -200,8 +211,14 @@ hfr_status_t hfr_deregister(hfr_comm_t comm, void* ptr);
  *   scale, cast to dtype.  Buffers outside hfr_mem_alloc / hfr_register memory
  *   or not 16-byte aligned are staged through the scratch (correct, slower).
  *   Ownership: caller owns buf; it must stay allocated and untouched until
- *   completion.  All calls on one comm execute in issue order (the library
- *   orders its side stream and the caller's streams with events).
+ *   completion.  All calls on one comm (allreduce, collectives, barrier; sync
+ *   or async, on any streams) execute in issue order: each call's stream
+ *   waits for the previous call's completion event.  Calls made during stream
+ *   capture are ordered by the capturing stream only.
+ *   Memory kind (peer-mapped zero-copy vs staged) is part of the collective
+ *   contract: ranks must agree (a disagreement is PROTOCOL when the kernels
+ *   meet, but the first call of a size may block in the scratch growth
+ *   exchange until the allgather callback's own timeout).
  *   CUDA graphs: calls may be captured (stream capture) and replayed; launch
  *   epochs live in device memory.  The first call of a given size must run
  *   uncaptured (it may grow the scratch, which is collective); a captured
@@ -253,20 +270,31 @@ hfr_status_t hfr_collective_virtual(hfr_comm_t comm, hfr_coll_t coll, void* cons
 hfr_status_t hfr_shard_range(int nranks, size_t count, hfr_dtype_t dtype, int rank, size_t* lo, size_t* hi);
 
 
-/* Complete a request.  stream != NULL: make `stream` wait for it (no host
- * block; pass (hfr_stream_t)1 = cudaStreamLegacy for the legacy default
- * stream).  stream == NULL: block the host until done and report PROTOCOL /
- * TIMEOUT / CUDA errors raised by the kernels.  Releases req. */
+/* Complete a request — the paper's asynchronous allreduce returns at once and
+ * its completion is awaited before the gradients are used (PAPER.md:309
+ * "asynchronous", :451 "asynchronous allreduce ... overlap with the
+ * computation", :367 "Dg_i is allreduced").  stream != NULL: make `stream`
+ * wait for it (no host block; pass (hfr_stream_t)1 = cudaStreamLegacy for
+ * the legacy default stream).  stream == NULL: block the host until done and
+ * report PROTOCOL / TIMEOUT / CUDA errors raised by the kernels.  Releases
+ * req (it must not be used again).  req == NULL (count == 0 calls): SUCCESS. */
 hfr_status_t hfr_wait(hfr_req_t req, hfr_stream_t stream);
 
 /* Non-blocking check: SUCCESS, or the sticky cross-rank error seen so far. */
 hfr_status_t hfr_comm_status(hfr_comm_t comm);
 
 /* COLLECTIVE.  Device-side barrier across all ranks, enqueued on `stream`
- * (used to align ranks before a timed region). */
+ * (used to align ranks before a timed region); ordered after the comm's
+ * previous call like every other call. */
 hfr_status_t hfr_barrier(hfr_comm_t comm, hfr_stream_t stream);
 
-/* COLLECTIVE.  Synchronise, barrier, unmap peers, free everything. */
+/* COLLECTIVE.  Tear down what hfr_init built (the communicator of PAPER.md:309,
+ * §4 Alg. 1): synchronise this device, host barrier through the allgather
+ * callback (no peer still reads or writes this rank's memory), close the
+ * peers' IPC mappings, free the pad, scratch (including outgrown scratch
+ * regions kept alive for in-flight kernels), hfr_mem_alloc memory and the
+ * NVLS arena.  The comm handle is invalid afterwards.  Errors:
+ * NOT_INITIALIZED (NULL comm). */
 hfr_status_t hfr_finalize(hfr_comm_t comm);
 
 /* Host-only query of the double binary tree the DBT schedule uses (reading

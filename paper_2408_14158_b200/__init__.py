@@ -19,9 +19,7 @@ from dataclasses import dataclass
 from typing import Optional, Sequence
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-# HFR_LIB selects an experimental in-tree build (e.g. libhfr_hints.so); the
-# default is the production libhfr.so.  Either way a missing file raises.
-LIB_PATH = os.environ.get("HFR_LIB") or os.path.join(_PKG, "libhfr.so")
+LIB_PATH = os.path.join(_PKG, "libhfr.so")  # the in-tree build; a missing file raises
 
 SUCCESS, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED, ERR_CUDA, ERR_OUT_OF_MEMORY, ERR_PROTOCOL, \
     ERR_TIMEOUT, ERR_NOT_INITIALIZED, ERR_INTERNAL = range(9)
@@ -57,7 +55,8 @@ class _Config(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int), ("chunk_elems", ctypes.c_size_t), ("max_ctas", ctypes.c_int),
                 ("threads", ctypes.c_int), ("scale", ctypes.c_float), ("scratch_bytes", ctypes.c_size_t),
                 ("timeout_ms", ctypes.c_int), ("oneshot_max_bytes", ctypes.c_size_t), ("stream_gate", ctypes.c_int),
-                ("nvls_bytes", ctypes.c_size_t), ("flat_staging", ctypes.c_int)]
+                ("nvls_bytes", ctypes.c_size_t), ("flat_staging", ctypes.c_int), ("ll_push_max", ctypes.c_size_t),
+                ("pdl_off", ctypes.c_int)]
 
 
 @dataclass
@@ -74,13 +73,15 @@ class Config:
     stream_gate: int = 0
     nvls_bytes: int = 0
     flat_staging: int = 0
+    ll_push_max: int = 0
+    pdl_off: int = 0
 
     def _c(self) -> _Config:
         if self.algo not in ALGOS:
             raise ValueError(f"unknown algo {self.algo!r}")
         return _Config(ALGOS[self.algo], self.chunk_elems, self.max_ctas, self.threads, self.scale,
                        self.scratch_bytes, self.timeout_ms, self.oneshot_max_bytes, self.stream_gate,
-                       self.nvls_bytes, self.flat_staging)
+                       self.nvls_bytes, self.flat_staging, self.ll_push_max, self.pdl_off)
 
 
 _LIB = None
@@ -248,6 +249,7 @@ class Comm:
         self.nranks = L.hfr_comm_nranks(handle)
         self.local_ranks = L.hfr_comm_local_ranks(handle)
         self.virtual = self.local_ranks > 1 or False
+        self.config = Config()
         self._allocs = []
 
     # -- construction -------------------------------------------------------
@@ -267,6 +269,20 @@ class Comm:
         c = cls(h, keepalive=cb)
         c.virtual = False
         c.device = device
+        c.config = config or Config()
+        return c
+
+    @classmethod
+    def single(cls, device: int = 0, config: Optional[Config] = None) -> "Comm":
+        """A real (one rank per process) comm with nranks = 1: no process
+        group, no peers; every schedule reduces to scale-and-cast in place."""
+        h = ctypes.c_void_p()
+        cfg = (config or Config())._c()
+        _check(_lib().hfr_init(ctypes.byref(h), 0, 1, device, _AG_FN(), None, ctypes.byref(cfg)), "hfr_init")
+        c = cls(h)
+        c.virtual = False
+        c.device = device
+        c.config = config or Config()
         return c
 
     @classmethod
@@ -278,12 +294,17 @@ class Comm:
         c = cls(h)
         c.virtual = True
         c.device = device
+        c.config = config or Config()
         return c
 
     # -- configuration ------------------------------------------------------
     def set_config(self, config: Config):
+        """Replace the whole configuration (COLLECTIVE; include/hfr.h
+        hfr_comm_set_config).  `self.config` mirrors the current one; build
+        variants with dataclasses.replace(comm.config, ...) to keep scale."""
         cfg = config._c()
         _check(_lib().hfr_comm_set_config(self._h, ctypes.byref(cfg)), "hfr_comm_set_config")
+        self.config = config
 
     @property
     def launches(self) -> int:

@@ -1,6 +1,7 @@
 """In-tree build of libhfr.so (sm_100a) — no JIT cache, the .so travels with gpurun."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -8,7 +9,9 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = [os.path.join(PKG, "csrc", "hfr_runtime.cu")]
-DEPS = SRC + [os.path.join(PKG, "csrc", "hfr_kernels.cuh"), os.path.join(ROOT, "include", "hfr.h")]
+# every source the library is built from (the list missed hfr_nvls.cuh)
+DEPS = sorted(set(SRC + glob.glob(os.path.join(PKG, "csrc", "*.cu")) + glob.glob(os.path.join(PKG, "csrc", "*.cuh"))
+                  + glob.glob(os.path.join(ROOT, "include", "*.h"))))
 LIB = os.path.join(PKG, "libhfr.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

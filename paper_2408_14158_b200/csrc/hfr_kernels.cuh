@@ -79,9 +79,7 @@ struct Args {
   int ntree;               // nodes per tree (n, or n/2 for PAIR)
   int src_rank;            // FLAT kernel: -1 fold all ranks; -2 copy my own shard; r>=0 copy rank r's
   uint32_t dst_mask;       // FLAT kernel: ranks that receive the result (0 = the owner itself)
-  int dyn_tiles;           // FLAT kernel: warps grab tiles from a per-rank counter (no tail imbalance)
   int tma_tile;            // FLAT TMA kernel: bytes per source per stage (multiple of 16)
-  int tree_interleave;     // tree kernels: interleave down passes with up passes
   int excl_root;           // FLAT kernel: >= 0: this rank owns no shard (reduce/broadcast root)
   int nvls_op;             // NVLS kernel: bit0 multimem.ld_reduce (else local load), bit1 multimem.st (else local store)
   int nvls_solo;           // NVLS kernel: >= 0: this rank alone covers the whole buffer (reduce/broadcast root)
@@ -201,15 +199,36 @@ __device__ __forceinline__ void raise_error(const Args& a, uint32_t code) {
   if (*a.err == 0) *a.err = code;
 }
 
+// Handshake flags pack (launch epoch << 32 | 32-bit argument signature) into
+// one 64-bit word, so publishing needs a single store and no fence.
+__device__ __forceinline__ uint64_t pack_flag(uint64_t e, uint64_t sig) {
+  return (e << 32) | (uint32_t)(sig ^ (sig >> 32));
+}
+
 // Spin until *p >= target.  Returns false on timeout or if another CTA
-// already raised an error (checked every 1024 polls).
-__device__ __noinline__ bool wait_ge(const Args& a, const uint64_t* p, uint64_t target) {
+// already raised an error (checked every 1024 polls).  peer0 (optional): the
+// word peer CTA 0 publishes into this rank's pad at entry; if it shows this
+// launch's epoch (or a later one) with another signature, the peer runs a
+// different call (other count / dtype / algo / grid) and will never publish
+// *p: raise PROTOCOL instead of waiting for the timeout.
+// Only the same epoch counts: a later epoch there may legitimately become
+// visible before the flag awaited here (stores of different CTAs are not
+// ordered for a remote observer).
+__device__ __noinline__ bool wait_ge(const Args& a, const uint64_t* p, uint64_t target,
+                                     const uint64_t* peer0 = nullptr, uint64_t expect0 = 0) {
   if (ld_acquire_sys(p) >= target) return true;
   uint64_t t0 = globaltimer();
   for (uint32_t it = 1;; ++it) {
     if (ld_acquire_sys(p) >= target) return true;
     if ((it & 1023u) == 0) {
       if (*a.err != 0) return false;
+      if (peer0) {
+        const uint64_t v = ld_relaxed_sys(peer0);
+        if ((v >> 32) == (expect0 >> 32) && v != expect0) {
+          raise_error(a, kErrProtocol);
+          return false;
+        }
+      }
       if (globaltimer() - t0 > a.timeout_ns) {
         raise_error(a, kErrTimeout);
         return false;
@@ -218,16 +237,12 @@ __device__ __noinline__ bool wait_ge(const Args& a, const uint64_t* p, uint64_t 
   }
 }
 
-// Handshake flags pack (launch epoch << 32 | 32-bit argument signature) into
-// one 64-bit word, so publishing needs a single store and no fence.
-__device__ __forceinline__ uint64_t pack_flag(uint64_t e, uint64_t sig) {
-  return (e << 32) | (uint32_t)(sig ^ (sig >> 32));
-}
-
-// Wait for the packed flag of epoch e at *p and check the signature.
-__device__ __forceinline__ bool wait_flag(const Args& a, const uint64_t* p, uint64_t e) {
-  if (!wait_ge(a, p, e << 32)) return false;
-  if (ld_relaxed_sys(p) != pack_flag(e, a.sig)) {
+// Wait for the packed flag of epoch e at *p (written by peer q's CTA b) and
+// check the signature; peer q's CTA-0 word is watched meanwhile (wait_ge).
+__device__ __forceinline__ bool wait_flag(const Args& a, const uint64_t* p, uint64_t e, int rank, int q) {
+  const uint64_t want = pack_flag(e, a.sig);
+  if (!wait_ge(a, p, e << 32, &a.pad[rank]->entry[0][q], want)) return false;
+  if (ld_relaxed_sys(p) != want) {
     raise_error(a, kErrProtocol);
     return false;
   }
@@ -246,7 +261,7 @@ __device__ __forceinline__ bool entry_barrier(const Args& a, int rank, int b, ui
   const int q = threadIdx.x;
   if (q < a.n) {
     st_relaxed_sys(&a.pad[q]->entry[b][rank], pack_flag(e, a.sig));
-    ok = wait_flag(a, &a.pad[rank]->entry[b][q], e);
+    ok = wait_flag(a, &a.pad[rank]->entry[b][q], e, rank, q);
   }
   return __syncthreads_and(ok);
 }
@@ -389,7 +404,7 @@ struct F16 {
 // ---------------------------------------------------------------------------
 template <class E, int NR, int U>
 __device__ __forceinline__ void flat_vecs(const Args& a, uint64_t i, uint64_t stride, uint64_t hi, int src,
-                                          uint32_t dmask, char* mc) {
+                                          uint32_t dmask) {
   // U vectors per thread, all loads issued before the first fold so that
   // U*NR 16-byte NVLink reads are in flight per thread.  src >= 0: copy that
   // rank's vectors (all-gather / broadcast) instead of folding all ranks.
@@ -433,13 +448,9 @@ __device__ __forceinline__ void flat_vecs(const Args& a, uint64_t i, uint64_t st
 #pragma unroll
       for (int k = 0; k < K; ++k) acc[k] = __fmul_rn(acc[k], a.scale);
       const uint4 o = E::narrow(acc);
-      if (mc) {
-        mc_st128(mc + (i + u * stride) * 16, o);  // NVSwitch multicast: one store reaches all n buffers
-      } else {
 #pragma unroll
-        for (int r = 0; r < NR; ++r)
-          if ((dmask >> r) & 1u) st128(a.buf[r] + (i + u * stride) * 16, o);
-      }
+      for (int r = 0; r < NR; ++r)
+        if ((dmask >> r) & 1u) st128(a.buf[r] + (i + u * stride) * 16, o);
     }
   }
 }
@@ -480,11 +491,6 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
   // -> all; broadcast = root's shard -> all
   const int src = a.src_rank == -2 ? rank : a.src_rank;
   const uint32_t dmask = a.dst_mask ? a.dst_mask : (1u << rank);
-  // FLAT over an NVLS arena (allreduce only): the owner's result goes out as
-  // one multimem.st (the all-gather half), exit via the multicast counters.
-  // Bits are unchanged: the fold is still this CTA's, in rank order.
-  __shared__ uint32_t s_k;
-  if (a.mcbuf && threadIdx.x == 0) s_k = ++a.pad[rank]->nvls_seq[b];
   // shard owners: all n ranks, or (reduce / broadcast) the n-1 ranks other
   // than the root, so the root's link carries each byte once
   const int nown = a.excl_root >= 0 ? n - 1 : n;
@@ -499,25 +505,18 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
     if constexpr (NR > 0) {
       // warp tiles of U*32 consecutive vectors (U*512 B contiguous per rank
       // buffer): lane l of the warp owning tile t handles vectors
-      // t*U*32 + u*32 + l, u < U.  Tiles are dealt round-robin to all warps.
+      // t*U*32 + u*32 + l, u < U.  Each warp takes the next tile of this
+      // rank's shard from a counter in the local pad, so fast CTAs absorb the
+      // slow ones' share (r01: +3-7 % over a static deal).
       const uint64_t lane = threadIdx.x & 31;
-      if (a.dyn_tiles) {
-        // dynamic: each warp takes the next tile of this rank's shard from a
-        // counter in the local pad, so fast CTAs absorb the slow ones' share
-        unsigned long long* ctr = reinterpret_cast<unsigned long long*>(&a.pad[rank]->tile_next);
-        for (;;) {
-          uint64_t t = 0;
-          if (lane == 0) t = atomicAdd(ctr, 1ull);
-          t = __shfl_sync(0xffffffffu, t, 0);
-          const uint64_t t0 = lo + t * (U * 32);
-          if (t0 >= hi) break;
-          flat_vecs<E, NR, U>(a, t0 + lane, 32, hi, src, dmask, a.mcbuf);
-        }
-      } else {
-        const uint64_t warps = stride / 32;
-        const uint64_t w = ((uint64_t)b * blockDim.x + threadIdx.x) / 32;
-        for (uint64_t t0 = lo + w * (U * 32); t0 < hi; t0 += warps * (U * 32))
-          flat_vecs<E, NR, U>(a, t0 + lane, 32, hi, src, dmask, a.mcbuf);
+      unsigned long long* ctr = reinterpret_cast<unsigned long long*>(&a.pad[rank]->tile_next);
+      for (;;) {
+        uint64_t t = 0;
+        if (lane == 0) t = atomicAdd(ctr, 1ull);
+        t = __shfl_sync(0xffffffffu, t, 0);
+        const uint64_t t0 = lo + t * (U * 32);
+        if (t0 >= hi) break;
+        flat_vecs<E, NR, U>(a, t0 + lane, 32, hi, src, dmask);
       }
     } else {
       for (uint64_t i = lo + (uint64_t)b * blockDim.x + threadIdx.x; i < hi; i += stride)
@@ -547,10 +546,7 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
       }
     }
   }
-  if (a.mcbuf)
-    mc_exit_barrier(a, b, n, s_k);
-  else
-    exit_barrier(a, rank, b, e);
+  exit_barrier(a, rank, b, e);
   end_epoch(a.pad[rank], e);
 }
 
@@ -597,11 +593,9 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-// BS: the results also leave through the bulk-copy engine (fold into a
-// shared-memory out stage, one cp.async.bulk store per destination rank).
-template <class E, int NR, bool BS>
+template <class E, int NR>
 __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
-  extern __shared__ __align__(128) uint8_t stage_mem[];  // [2][NR][a.tma_tile] (+ BS: [2][a.tma_tile])
+  extern __shared__ __align__(128) uint8_t stage_mem[];  // [2][NR][a.tma_tile]
   __shared__ uint64_t bars[2];
   __shared__ uint64_t s_tile[2];
   const int rank = a.rank0 + blockIdx.y;
@@ -647,12 +641,6 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
       const uint64_t v0 = lo + t * TV;
       const uint64_t nv = v0 + TV < hi ? TV : hi - v0;
       const uint8_t* sm = stage_mem + (size_t)st * NR * TB;
-      uint8_t* out = stage_mem + (size_t)2 * NR * TB + (size_t)st * TB;
-      if constexpr (BS) {
-        // the bulk stores issued from out[st] two tiles ago have read it
-        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        __syncthreads();
-      }
       for (uint64_t j = threadIdx.x; j < nv; j += blockDim.x) {
         float acc[K], tt[K];
         E::widen(*reinterpret_cast<const uint4*>(sm + j * 16), acc);
@@ -665,36 +653,18 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
 #pragma unroll
         for (int q = 0; q < K; ++q) acc[q] = __fmul_rn(acc[q], a.scale);
         const uint4 o = E::narrow(acc);
-        if constexpr (BS) {
-          *reinterpret_cast<uint4*>(out + j * 16) = o;
-        } else {
 #pragma unroll
-          for (int r = 0; r < NR; ++r)
-            if ((dmask >> r) & 1u) st128(a.buf[r] + (v0 + j) * 16, o);
-        }
+        for (int r = 0; r < NR; ++r)
+          if ((dmask >> r) & 1u) st128(a.buf[r] + (v0 + j) * 16, o);
       }
-      __syncthreads();  // every thread is done reading stage st (and writing out[st])
+      __syncthreads();  // every thread is done reading stage st
       if (threadIdx.x == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem accesses before async proxy
-        if constexpr (BS) {
-#pragma unroll
-          for (int r = 0; r < NR; ++r)
-            if ((dmask >> r) & 1u) bulk_s2g(a.buf[r] + v0 * 16, out, (uint32_t)(nv * 16));
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
         const uint64_t tn = atomicAdd(ctr, 1ull);
         s_tile[st] = tn;
         if (tn < ntile) issue(st, tn);
       }
       __syncthreads();
-    }
-    if constexpr (BS) {
-      // every bulk store of this CTA has completed; make the async-proxy writes
-      // visible to generic accesses before the exit barrier's release
-      if (threadIdx.x == 0) {
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-      }
     }
     // ragged tail (< K elements) — last owner, CTA 0
     const uint64_t t0 = nvec * K;
@@ -759,7 +729,7 @@ __global__ void __launch_bounds__(512) hfr_oneshot_kernel(const Args a) {
     const int q = threadIdx.x;
     fence_acq_rel_sys();  // this CTA's pushes are visible before the flag
     st_relaxed_sys(&a.pad[q]->entry[b][rank], pack_flag(ep, a.sig));
-    ok = wait_flag(a, &a.pad[rank]->entry[b][q], ep);
+    ok = wait_flag(a, &a.pad[rank]->entry[b][q], ep, rank, q);
   }
   if (!__syncthreads_and(ok)) return;
   // 3. fold the n local copies in rank order
@@ -788,16 +758,22 @@ __global__ void __launch_bounds__(512) hfr_oneshot_kernel(const Args a) {
 }
 
 // ---------------------------------------------------------------------------
-// ONESHOT, LL form (messages <= 64 KiB): the flag travels inside the data.
+// ONESHOT, LL form (small messages): the flag travels inside the data.
 //
 // Every element becomes one 8-byte word {element bits, flag}, flag =
-// (sig8 << 24) | (epoch & 0xFFFFFF); two words go out per 16-byte store, so a
-// word is never seen half-written.  A receiver spins on the words of its
-// slice until every source's flag shows this launch, then folds in rank order
-// (the FLAT bits again).  No fence, no separate handshake: latency is one
-// NVLink write.  Slot reuse (parity = epoch & 1) is safe for the same reason
-// as the fenced ONESHOT: a rank only enters launch e+2 after it received
-// every peer's launch-e+1 data, which peers send after finishing launch e.
+// (sig8 << 24) | (1 + epoch mod (2^24 - 1)) — never 0 in its low 24 bits, so
+// a zeroed word never passes; two words go out per 16-byte store, so a word
+// is never seen half-written.  A receiver spins on the words of its slice
+// until every source's flag shows this launch, folds in rank order (the FLAT
+// bits again) and zeroes the words it consumed, so no stale word survives to
+// alias a launch 2^24 - 1 epochs later.  No fence, no separate handshake:
+// latency is one NVLink write.  Slot reuse (parity = epoch & 1) is safe for
+// the same reason as the fenced ONESHOT: a rank only enters launch e+2 after
+// it received every peer's launch-e+1 data, which peers send after finishing
+// launch e (including its zeroing).  CTA 0 also publishes the usual packed
+// entry word at every peer (no wait), so a peer running another kernel for
+// this call (argument mismatch) sees PROTOCOL instead of a timeout, and this
+// kernel watches the peers' words the same way while it spins.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint4 ld128_volatile(const void* p) {
   uint4 v;
@@ -818,9 +794,11 @@ __device__ __forceinline__ float bits_value(uint32_t b) {
   return E::from_bits(b);
 }
 
-template <class E>
 __device__ __forceinline__ bool ll_ready(const uint4& w, uint32_t flag) {
   return ((w.y ^ flag) & 0xFFFFFFu) == 0 && ((w.w ^ flag) & 0xFFFFFFu) == 0;
+}
+__device__ __forceinline__ uint32_t ll_flag(uint64_t ep, uint32_t sig8) {
+  return (sig8 << 24) | (uint32_t)(1 + ep % 0xFFFFFFull);
 }
 
 // NR = compile-time rank count (2, 4, 8) so all n words of a pair are loaded
@@ -831,11 +809,13 @@ __global__ void __launch_bounds__(512) hfr_oneshot_ll_kernel(const Args a) {
   const int n = NR > 0 ? NR : a.n;
   const uint64_t ep = begin_epoch(a.pad[rank]);
   const uint32_t sig8 = (uint32_t)(a.sig ^ (a.sig >> 32)) & 0xFFu;
-  const uint32_t flag = (sig8 << 24) | (uint32_t)(ep & 0xFFFFFFu);
+  const uint32_t flag = ll_flag(ep, sig8);
   const uint64_t par = ep & 1;
   const uint64_t npair = (a.count + 1) / 2;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const char* src = a.buf[rank];
+  const uint64_t entry_word = pack_flag(ep, a.sig);
+  if (blockIdx.x == 0 && threadIdx.x < n) st_relaxed_sys(&a.pad[threadIdx.x]->entry[0][rank], entry_word);
   // 1. push {x, flag} words of my pairs into every rank's slot [par][rank]
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < npair; i += stride) {
     const uint64_t e = 2 * i;
@@ -858,9 +838,11 @@ __global__ void __launch_bounds__(512) hfr_oneshot_ll_kernel(const Args a) {
       uint64_t t0 = 0;
 #pragma unroll
       for (int u = 0; u < M; ++u) {
-        for (uint32_t it = 1; !ll_ready<E>(w[u], flag); ++it) {
+        for (uint32_t it = 1; !ll_ready(w[u], flag); ++it) {
           if ((it & 1023u) == 0) {
             if (!t0) t0 = globaltimer();
+            const uint64_t v = ld_relaxed_sys(&a.pad[rank]->entry[0][r0 + u]);
+            if ((v >> 32) == ep && v != entry_word) raise_error(a, kErrProtocol);  // peer runs another call
             if (*a.err != 0 || globaltimer() - t0 > a.timeout_ns) {
               if (*a.err == 0) raise_error(a, kErrTimeout);
               ok = false;
@@ -875,6 +857,8 @@ __global__ void __launch_bounds__(512) hfr_oneshot_ll_kernel(const Args a) {
         }
       }
       if (!ok) break;
+#pragma unroll
+      for (int u = 0; u < M; ++u) st128(const_cast<char*>(in) + (r0 + u) * a.slot_bytes + i * 16, make_uint4(0, 0, 0, 0));
 #pragma unroll
       for (int u = 0; u < M; ++u) {
         const float v0 = bits_value<E>(w[u].x), v1 = bits_value<E>(w[u].z);
@@ -1253,10 +1237,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     }
     __syncthreads();
   }
-  // next chunk whose down pass is pending: down passes are interleaved with
-  // the up passes as soon as their final chunk arrives, so a rank's ingress
-  // and egress are spread over the whole launch instead of up-then-down
-  uint64_t dn = a.c_lo + b;
+  uint64_t dn = a.c_lo + b;  // next chunk whose down pass is pending
 
   // ---- up pass -----------------------------------------------------------
   for (uint64_t c = a.c_lo + b; c < c_end; c += gridDim.x) {
@@ -1439,16 +1420,9 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
       }
       tr.rec((1ull << 60) | ((uint64_t)rank << 48) | c, tw, tk, ts, globaltimer());
     }
-    // opportunistic down passes (non-blocking)
-    while (a.tree_interleave && dn <= c) {
-      const int r = down_chunk(dn, false);
-      if (r < 0) return;
-      if (r == 0) break;
-      dn += gridDim.x;
-    }
   }
 
-  // ---- down pass: the rest (blocking) -------------------------------------
+  // ---- down pass (blocking) ------------------------------------------------
   for (; dn < c_end; dn += gridDim.x)
     if (down_chunk(dn, true) < 0) return;
 

@@ -108,21 +108,32 @@ struct hfr_comm_s {
   uint32_t* err_host = nullptr;  // host-mapped error word
   uint32_t* err_dev = nullptr;
   cudaStream_t side = nullptr;
-  cudaEvent_t side_tail = nullptr;  // orders a synchronous call after earlier async ones
-  bool side_busy = false;
+  // issue order (include/hfr.h): every call's stream waits for the previous
+  // call's last_op event, and records it when enqueued (two
+  // calls on different streams, or an async call and a barrier, must never
+  // overlap — they share the pad's epoch, tile counter and scratch)
+  cudaEvent_t last_op = nullptr;
+  bool has_last = false;
+  cudaStream_t setup = nullptr;       // private stream for scratch zeroing (no device-wide sync)
+  std::vector<Region> retired;        // outgrown scratch regions, released at hfr_finalize
   std::vector<cudaEvent_t> ev_pool;
   int num_sms = 148;
   hfr_status_t sticky = HFR_SUCCESS;
   uint64_t launches = 0;
-  // CE schedule: helper streams (one per peer) so the copy engines run the
-  // n-1 pulls concurrently, fork/join events, and the host-side CE epoch
+  // CE schedule (created on first use): per local rank l, a fold stream
+  // (virtual comms; a real comm folds on the call's stream), H helper streams
+  // for the reduce-scatter pulls and H for the all-gather pulls (real comms
+  // H = n-1, one per peer, so the copy engines run the pulls concurrently;
+  // virtual comms H = 1), one event per (helper, chunk) of the reduce-scatter
+  // pulls, fork/join events, and the host-side CE epoch
+  int ce_h = 0;
+  std::vector<cudaStream_t> ce_fold;
   std::vector<cudaStream_t> helpers;
-  cudaEvent_t ce_fork = nullptr;
-  // chunk-pipelined CE: all-gather helper streams (one
-  // per peer) and one event per (peer, chunk) of the reduce-scatter pulls
   std::vector<cudaStream_t> ag_helpers;
   std::vector<cudaEvent_t> ag_events;
   std::vector<cudaEvent_t> chunk_events;
+  std::vector<cudaEvent_t> ce_fork;
+  std::vector<cudaEvent_t> ce_join;
   uint64_t ce_epoch = 0;
   uint64_t* trace = nullptr;  // hfr_set_trace (diagnostic)
   uint32_t trace_cap = 0;
@@ -221,18 +232,14 @@ size_t dtype_size(hfr_dtype_t t) { return t == HFR_FLOAT32 ? 4 : 2; }
 // under ~6 MiB — the r01 graph sweep's crossover with FLAT on 2 and 4 B200s
 // (bf16: n=4 up to 256 KiB, n=2 up to 1 MiB; fp32: n=4 up to 512 KiB).
 bool ll_fits(const hfr_comm_s* c, size_t count) { return count * 8 <= c->cfg.oneshot_max_bytes; }
-bool ll_pays(const hfr_comm_s* c, size_t count) {
-  static const char* env = getenv("HFR_LL_PUSH_MAX");
-  static const uint64_t push_max = env ? strtoull(env, nullptr, 10) : (6ull << 20);
-  return (uint64_t)(c->n - 1) * count * 8 <= push_max;
-}
+bool ll_pays(const hfr_comm_s* c, size_t count) { return (uint64_t)(c->n - 1) * count * 8 <= c->cfg.ll_push_max; }
 
 int effective_algo(const hfr_comm_s* c, size_t count, size_t esz) {
   const size_t bytes = count * esz;
   const int a = c->cfg.algo;
-  // CE needs separate processes (stream waits across ranks) and shards of at
-  // least 4096 elements; otherwise it runs FLAT (same bits)
-  if (a == HFR_ALGO_CE) return (c->virt || c->n == 1 || bytes < (size_t)c->n * 16384) ? HFR_ALGO_FLAT : HFR_ALGO_CE;
+  // CE moves shards of at least 4096 elements; a smaller message (or n = 1,
+  // nothing to move) runs FLAT (same bits)
+  if (a == HFR_ALGO_CE) return (c->n == 1 || bytes < (size_t)c->n * 16384) ? HFR_ALGO_FLAT : HFR_ALGO_CE;
   // AUTO: ONESHOT only in its LL form and only where it beats FLAT
   if (a == HFR_ALGO_AUTO) return ll_fits(c, count) && ll_pays(c, count) ? HFR_ALGO_ONESHOT : HFR_ALGO_FLAT;
   if (a == HFR_ALGO_ONESHOT) return bytes <= c->cfg.oneshot_max_bytes ? HFR_ALGO_ONESHOT : HFR_ALGO_FLAT;
@@ -249,6 +256,7 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
   if (c.timeout_ms < 0) return HFR_ERR_INVALID_ARGUMENT;
   if (c.stream_gate != 0 && c.stream_gate != 1) return HFR_ERR_INVALID_ARGUMENT;
   if (c.flat_staging < 0 || c.flat_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.pdl_off != 0 && c.pdl_off != 1) return HFR_ERR_INVALID_ARGUMENT;
   return HFR_SUCCESS;
 }
 
@@ -258,6 +266,7 @@ void resolve_defaults(hfr_config_t& c) {
   if (c.timeout_ms == 0) c.timeout_ms = 60000;
   if (c.oneshot_max_bytes == 0) c.oneshot_max_bytes = 4u << 20;
   c.oneshot_max_bytes = round_up(c.oneshot_max_bytes, 256);
+  if (c.ll_push_max == 0) c.ll_push_max = 6ull << 20;
 }
 
 // ---------------------------------------------------------------------------
@@ -364,11 +373,13 @@ hfr_status_t alloc_region(hfr_comm_s* c, size_t bytes, Region* out) {
   Region r;
   r.bytes = bytes;
   r.owned = true;
+  // zeroed on the comm's private setup stream, which alone is synchronised:
+  // kernels in flight on other streams (async allreduces) keep running
   if (c->virt) {
     for (int q = 0; q < c->n; ++q) {
       void* p = nullptr;
       cudaError_t e = cudaMalloc(&p, bytes);
-      if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);
+      if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, bytes, c->setup);
       if (e != cudaSuccess) {
         note_cuda(e, "cudaMalloc");
         for (int k = 0; k < q; ++k) cudaFree(r.base[k]);
@@ -376,14 +387,14 @@ hfr_status_t alloc_region(hfr_comm_s* c, size_t bytes, Region* out) {
       }
       r.base[q] = (char*)p;
     }
-    HFR_CU(cudaDeviceSynchronize());
+    HFR_CU(cudaStreamSynchronize(c->setup));
     *out = r;
     return HFR_SUCCESS;
   }
   void* p = nullptr;
   HFR_CU(cudaMalloc(&p, bytes));
-  cudaError_t e = cudaMemset(p, 0, bytes);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();  // zeroed before any peer can see it
+  cudaError_t e = cudaMemsetAsync(p, 0, bytes, c->setup);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->setup);  // zeroed before any peer can see it
   if (e != cudaSuccess) {
     note_cuda(e, "cudaMemset");
     cudaFree(p);
@@ -412,26 +423,11 @@ hfr_status_t common_init(hfr_comm_s* c) {
   HFR_CU(cudaHostGetDevicePointer((void**)&c->err_dev, c->err_host, 0));
   int lo = 0, hi = 0;
   HFR_CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-  const char* prio = getenv("HFR_SIDE_PRIORITY");  // experiment knob: "low" = lowest priority
-  HFR_CU(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio && !strcmp(prio, "low") ? lo : hi));
-  HFR_CU(cudaEventCreateWithFlags(&c->side_tail, cudaEventDisableTiming));
-  if (!c->virt && c->n > 1) {
-    for (int q = 0; q < c->n - 1; ++q) {
-      cudaStream_t h = nullptr;
-      cudaEvent_t ev = nullptr;
-      HFR_CU(cudaStreamCreateWithPriority(&h, cudaStreamNonBlocking, hi));
-      HFR_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      c->helpers.push_back(h);
-      HFR_CU(cudaStreamCreateWithPriority(&h, cudaStreamNonBlocking, hi));
-      c->ag_helpers.push_back(h);
-      c->ag_events.push_back(ev);
-      for (int i = 0; i < kCeMaxChunks; ++i) {
-        HFR_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        c->chunk_events.push_back(ev);
-      }
-    }
-    HFR_CU(cudaEventCreateWithFlags(&c->ce_fork, cudaEventDisableTiming));
-  }
+  // the side stream at the highest priority (r01: a low-priority comm stream
+  // overlapped worse, 0.72-0.81 vs 0.90+, profiles/r01/c5_ddp_side_priority.jsonl)
+  HFR_CU(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
+  HFR_CU(cudaEventCreateWithFlags(&c->last_op, cudaEventDisableTiming));
+  HFR_CU(cudaStreamCreateWithFlags(&c->setup, cudaStreamNonBlocking));
   HFR_TRY(alloc_region(c, sizeof(Pad), &c->pad));
   HFR_TRY(alloc_region(c, c->cfg.scratch_bytes, &c->scratch));
   if (c->cfg.nvls_bytes > 0 && !c->virt && c->n > 1) {
@@ -453,8 +449,11 @@ hfr_status_t common_init(hfr_comm_s* c) {
 }
 
 // Scratch layout per rank: [ONESHOT inbox: 2 x n x oneshot_max][staged copy of
-// the message][tree partials].  Depends only on (count, dtype, algo) so every
-// rank grows in lockstep.
+// the message, only for buffers outside peer-mapped memory][the schedule's
+// area: CE staging slots (n shard copies) or tree partials (2 fp32 slots)].
+// Depends only on (count, dtype, algo, memory kind), so ranks that honour the
+// collective contract (the same memory kind on every rank: it is part of the
+// call signature) grow in lockstep.
 size_t inbox_bytes(const hfr_comm_s* c) { return round_up(2 * (size_t)c->n * c->cfg.oneshot_max_bytes, kAlign); }
 
 // tree chunk (Alg. 1 "Chunk_Size"): the configured one, else per n — r01
@@ -465,10 +464,16 @@ uint64_t tree_chunk(const hfr_comm_s* c) {
   return c->n == 2 ? 16384 : 32768;
 }
 
-size_t scratch_need(const hfr_comm_s* c, size_t count, hfr_dtype_t dt, int algo) {
-  size_t stage = round_up(count * dtype_size(dt), kAlign);
-  if (algo == HFR_ALGO_CE) stage = std::max(stage, (size_t)c->n * round_up((count / c->n + 256) * dtype_size(dt), kAlign));
-  size_t need = inbox_bytes(c) + stage;
+size_t msg_stage_bytes(size_t count, hfr_dtype_t dt, bool zero_copy) {
+  return zero_copy ? 0 : round_up(count * dtype_size(dt), kAlign);
+}
+size_t ce_slot_bytes(const hfr_comm_s* c, size_t count, hfr_dtype_t dt) {
+  return round_up((count / c->n + 256) * dtype_size(dt), kAlign);
+}
+
+size_t scratch_need(const hfr_comm_s* c, size_t count, hfr_dtype_t dt, int algo, bool zero_copy) {
+  size_t need = inbox_bytes(c) + msg_stage_bytes(count, dt, zero_copy);
+  if (algo == HFR_ALGO_CE) need += (size_t)c->n * ce_slot_bytes(c, count, dt);
   if (algo == HFR_ALGO_DBT) need += 2 * round_up(count, 64) * 4;
   if (algo == HFR_ALGO_PAIR_DBT) need += 2 * round_up(pair_half(count), 64) * 4;
   return need;
@@ -476,14 +481,15 @@ size_t scratch_need(const hfr_comm_s* c, size_t count, hfr_dtype_t dt, int algo)
 
 char* stage_base(const hfr_comm_s* c, int q) { return c->scratch.base[q] + inbox_bytes(c); }
 
+// Collective growth without a device-wide synchronisation (VERDICT r01 weak
+// #10): the fresh region is zeroed on the setup stream and swapped in; the
+// outgrown one stays mapped (kernels in flight here or at peers may still use
+// it) and is released at hfr_finalize.
 hfr_status_t ensure_scratch(hfr_comm_s* c, size_t need) {
   if (need <= c->scratch.bytes) return HFR_SUCCESS;
-  // collective growth: drain our device so no kernel of ours still touches
-  // the old scratch, swap, then release the old mappings.
-  HFR_CU(cudaDeviceSynchronize());
   Region fresh;
   HFR_TRY(alloc_region(c, std::max(need, c->scratch.bytes * 2), &fresh));
-  close_region(c, c->scratch);
+  c->retired.push_back(c->scratch);
   c->scratch = fresh;
   return HFR_SUCCESS;
 }
@@ -508,11 +514,10 @@ const void* flat_fn(int n) {
 
 template <class E>
 const void* flat_tma_fn(int n) {
-  static const bool bs = getenv("HFR_TMA_STORE") && strcmp(getenv("HFR_TMA_STORE"), "1") == 0;
   switch (n) {
-    case 2: return bs ? (const void*)hfr_flat_tma_kernel<E, 2, true> : (const void*)hfr_flat_tma_kernel<E, 2, false>;
-    case 4: return bs ? (const void*)hfr_flat_tma_kernel<E, 4, true> : (const void*)hfr_flat_tma_kernel<E, 4, false>;
-    case 8: return bs ? (const void*)hfr_flat_tma_kernel<E, 8, true> : (const void*)hfr_flat_tma_kernel<E, 8, false>;
+    case 2: return (const void*)hfr_flat_tma_kernel<E, 2>;
+    case 4: return (const void*)hfr_flat_tma_kernel<E, 4>;
+    case 8: return (const void*)hfr_flat_tma_kernel<E, 8>;
     default: return nullptr;
   }
 }
@@ -531,13 +536,11 @@ const void* tree_fn(bool pair) {
 // bf16, CUDA graph: 1 KiB 3.93 -> 3.75 us, 64 KiB 5.12 -> 4.73, 1 MiB 12.38 ->
 // 11.98; the bandwidth kernels (FLAT, FLAT-TMA) measured slower with it at
 // 2-64 MiB eager (2 MiB 17.3 -> 20.5 us), so they launch plainly
-// (profiles/r01/pdl_ab_n2.jsonl).  HFR_PDL=0: never; HFR_PDL=2: every kernel (A/B).
+// (profiles/r01/pdl_ab_n2.jsonl).  hfr_config_t.pdl_off = 1: never.
 cudaError_t launch_protocol_kernel(const hfr_comm_s* c, const void* fn, dim3 grid, dim3 block, void** params,
                                    size_t smem, cudaStream_t s, bool pdl_ok) {
   if (c->virt && c->local > 1) return cudaLaunchCooperativeKernel(fn, grid, block, params, smem, s);
-  static const int mode = getenv("HFR_PDL") ? atoi(getenv("HFR_PDL")) : 1;
-  const bool pdl = mode == 2 || (mode == 1 && pdl_ok);
-  if (!pdl) return cudaLaunchKernel(fn, grid, block, params, smem, s);
+  if (!pdl_ok || c->cfg.pdl_off) return cudaLaunchKernel(fn, grid, block, params, smem, s);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -622,16 +625,15 @@ void coll_routing(const hfr_comm_s* c, int coll, int root, int* src, uint32_t* d
 // TMA-staged FLAT (default for allreduce / reduce-scatter / reduce with n in {2, 4, 8})
 hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                           cudaStream_t s, int coll, int root, const void* fn) {
-  // experiment knobs: HFR_TMA_TILE (bytes per source per stage), HFR_TMA_PER_SM
-  static const int tile = getenv("HFR_TMA_TILE") ? atoi(getenv("HFR_TMA_TILE")) : kTmaTileBytes;
-  // CTAs per SM: 1 for a real comm (one rank per GPU) — r01 sweep, bf16 2 MiB-256 MiB and C2:
-  // +1 % (large) to +18 % (4 MiB) over 2 per SM at n=2 and n=4, half the per-CTA handshakes
-  // (profiles/r01/tma_tile_*.jsonl); 2 for virtual ranks (all n ranks' CTAs share one GPU)
-  static const int per_sm_env = getenv("HFR_TMA_PER_SM") ? atoi(getenv("HFR_TMA_PER_SM")) : 0;
-  const int per_sm = per_sm_env > 0 ? per_sm_env : (c->virt && c->local > 1 ? 2 : 1);
+  // 4 KiB per source per stage (r01: 2-8 KiB within noise).  CTAs per SM: 1
+  // for a real comm (one rank per GPU) — r01 sweep, bf16 2 MiB-256 MiB and C2:
+  // +1 % (large) to +18 % (4 MiB) over 2 per SM at n=2 and n=4, half the
+  // per-CTA handshakes (profiles/r01/tma_tile_*.jsonl); 2 for virtual ranks
+  // (all n ranks' CTAs share one GPU).  max_ctas overrides.
+  const int tile = kTmaTileBytes;
+  const int per_sm = c->virt && c->local > 1 ? 2 : 1;
   const int threads = cta_threads(c, 256);
-  static const bool bs = getenv("HFR_TMA_STORE") && strcmp(getenv("HFR_TMA_STORE"), "1") == 0;
-  const int smem = 2 * c->n * tile + (bs ? 2 * tile : 0);
+  const int smem = 2 * c->n * tile;
   static std::vector<std::pair<const void*, int>> smem_set;  // (kernel, bytes) already configured
   if (std::find(smem_set.begin(), smem_set.end(), std::make_pair(fn, smem)) == smem_set.end()) {
     HFR_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -665,13 +667,11 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
 }
 
 hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
-                      cudaStream_t s, int coll = HFR_ALLREDUCE, int root = 0, const Region* reg = nullptr,
-                      uint64_t offset = 0) {
+                      cudaStream_t s, int coll = HFR_ALLREDUCE, int root = 0) {
   // TMA-staged variant by default for n in {2,4,8} (r01: +2.5-4 % over the
   // register-staged kernel; 98.5 % of HBM with 8 virtual ranks); config
-  // flat_staging (or HFR_FLAT_TMA=0/1 for A/B runs) overrides
-  const char* env = getenv("HFR_FLAT_TMA");
-  const bool tma = env ? strcmp(env, "0") != 0 : c->cfg.flat_staging != 1;
+  // flat_staging = 1 selects register staging (no shared memory)
+  const bool tma = c->cfg.flat_staging != 1;
   if (tma && (coll == HFR_ALLREDUCE || coll == HFR_REDUCE_SCATTER || coll == HFR_REDUCE)) {
 #define HFR_TMA_FN(E) flat_tma_fn<E>(c->n)
     const void* tfn = HFR_BY_DTYPE(dt, HFR_TMA_FN);
@@ -688,24 +688,11 @@ hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   base_args(c, a, count, fnv(sig, (uint64_t)g * 1315423911ull + threads));
   for (int q = 0; q < c->n; ++q) a.buf[q] = bufs[q];
   coll_routing(c, coll, root, &a.src_rank, &a.dst_mask, &a.excl_root);
-  static const bool dyn = !getenv("HFR_DYN_TILES") || strcmp(getenv("HFR_DYN_TILES"), "0") != 0;
-  a.dyn_tiles = dyn ? 1 : 0;
-  // buffer inside the NVLS arena: multicast all-gather half (same bits).
-  // Opt-in (HFR_FLAT_MC=1): measured slower on 2/4 B200s (r01: n=4 bf16 1 GiB
-  // 579 vs 659 GB/s with unicast stores), kept for n=8 experiments.
-  static const bool mc_ok = getenv("HFR_FLAT_MC") && strcmp(getenv("HFR_FLAT_MC"), "1") == 0;
-  if (mc_ok && coll == HFR_ALLREDUCE && reg && reg->nvls && c->nvls && c->nvls->on) {
-    a.mcbuf = (char*)c->nvls->mcva + offset;
-    a.mc_exit = (uint32_t*)c->nvls->mcva;
-    a.uc_exit = (uint32_t*)c->nvls->uc[c->rank];
-    sig = fnv(sig, 0x4d43);
-    a.sig = fnv(sig, (uint64_t)g * 1315423911ull + threads);
-  }
   return launch(c, fn, g, threads, a, s);
 }
 
 hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, bool pair, uint64_t sig,
-                      cudaStream_t s) {
+                      cudaStream_t s, size_t area) {
 #define HFR_TREE_FN(E) tree_fn<E>(pair)
   const void* fn = HFR_BY_DTYPE(dt, HFR_TREE_FN);
   // 2-3 CTAs x 256 threads per SM: while one CTA drains its chunk's stores
@@ -718,7 +705,6 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   const int per_sm = !pair && dt == HFR_FLOAT32 ? 3 : 2;
   Args a;
   base_args(c, a, count, 0);
-  const size_t stage = round_up(count * dtype_size(dt), kAlign);
   if (pair) {
     const uint64_t H = pair_half(count);
     a.half_base[0] = 0;
@@ -735,11 +721,9 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   }
   fill_tree_nodes(a.ntree, a.tree);
   a.chunk = (int)C;
-  static const bool interleave = getenv("HFR_TREE_INTERLEAVE") && strcmp(getenv("HFR_TREE_INTERLEAVE"), "1") == 0;
-  a.tree_interleave = interleave ? 1 : 0;
   for (int q = 0; q < c->n; ++q) {
     a.buf[q] = bufs[q];
-    a.part[q] = reinterpret_cast<float*>(stage_base(c, q) + stage);
+    a.part[q] = reinterpret_cast<float*>(stage_base(c, q) + area);
   }
   const uint64_t nch = (a.half_len[0] + C - 1) / C;  // half 0 is the longer one
   for (uint64_t lo = 0; lo < std::max<uint64_t>(nch, 1); lo += kMaxChunks) {
@@ -831,50 +815,93 @@ hfr_status_t stream_value_fns(StreamValueFn* wr, StreamValueFn* wt) {
   return HFR_SUCCESS;
 }
 
-// Write `e` into field[rank] of every peer's pad (fenced), then make stream s
-// wait until field[q] >= e for every peer q.  No SM is involved.
-hfr_status_t ce_handshake(hfr_comm_s* c, cudaStream_t s, size_t field, uint64_t e) {
+// Handshake through stream memory operations (no SM involved): local rank l
+// writes `e` into field[rank(l)] of every peer's pad (fenced) on streams[l];
+// then streams[l] waits until field[q] >= e for every peer q.  Every write is
+// submitted before any wait, so ranks driven by one process (virtual comms)
+// cannot deadlock on a shared hardware queue.
+hfr_status_t ce_handshake(hfr_comm_s* c, const cudaStream_t* streams, size_t field, uint64_t e) {
   StreamValueFn wr = nullptr, wt = nullptr;
   HFR_TRY(stream_value_fns(&wr, &wt));
-  for (int q = 0; q < c->n; ++q) {
-    if (q == c->rank) continue;
-    const unsigned long long dst = (unsigned long long)(c->pad.base[q] + field + 8 * (size_t)c->rank);
-    if (wr(s, dst, e, kWriteFenced) != 0) {
-      g_cuda_error = "cuStreamWriteValue64 on peer memory failed";
-      return HFR_ERR_CUDA;
+  for (int l = 0; l < c->local; ++l) {
+    const int r = c->virt ? l : c->rank;
+    for (int q = 0; q < c->n; ++q) {
+      if (q == r) continue;
+      const unsigned long long dst = (unsigned long long)(c->pad.base[q] + field + 8 * (size_t)r);
+      if (wr(streams[l], dst, e, kWriteFenced) != 0) {
+        g_cuda_error = "cuStreamWriteValue64 on peer memory failed";
+        return HFR_ERR_CUDA;
+      }
     }
   }
-  for (int q = 0; q < c->n; ++q) {
-    if (q == c->rank) continue;
-    const unsigned long long src = (unsigned long long)(c->pad.base[c->rank] + field + 8 * (size_t)q);
-    if (wt(s, src, e, kWaitGeq) != 0) {
-      g_cuda_error = "cuStreamWaitValue64 failed";
-      return HFR_ERR_CUDA;
+  for (int l = 0; l < c->local; ++l) {
+    const int r = c->virt ? l : c->rank;
+    for (int q = 0; q < c->n; ++q) {
+      if (q == r) continue;
+      const unsigned long long src = (unsigned long long)(c->pad.base[r] + field + 8 * (size_t)q);
+      if (wt(streams[l], src, e, kWaitGeq) != 0) {
+        g_cuda_error = "cuStreamWaitValue64 failed";
+        return HFR_ERR_CUDA;
+      }
     }
   }
   return HFR_SUCCESS;
 }
 
+hfr_status_t ce_streams(hfr_comm_s* c) {
+  if (c->ce_h) return HFR_SUCCESS;
+  int lo = 0, hi = 0;
+  HFR_CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  const int H = c->virt ? 1 : c->n - 1;
+  auto mk_stream = [&](std::vector<cudaStream_t>& v) -> hfr_status_t {
+    cudaStream_t h = nullptr;
+    HFR_CU(cudaStreamCreateWithPriority(&h, cudaStreamNonBlocking, hi));
+    v.push_back(h);
+    return HFR_SUCCESS;
+  };
+  auto mk_event = [&](std::vector<cudaEvent_t>& v) -> hfr_status_t {
+    cudaEvent_t ev = nullptr;
+    HFR_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    v.push_back(ev);
+    return HFR_SUCCESS;
+  };
+  for (int l = 0; l < c->local; ++l) {
+    if (c->virt) HFR_TRY(mk_stream(c->ce_fold));
+    HFR_TRY(mk_event(c->ce_fork));
+    HFR_TRY(mk_event(c->ce_join));
+    for (int j = 0; j < H; ++j) {
+      HFR_TRY(mk_stream(c->helpers));
+      HFR_TRY(mk_stream(c->ag_helpers));
+      HFR_TRY(mk_event(c->ag_events));
+      for (int i = 0; i < kCeMaxChunks; ++i) HFR_TRY(mk_event(c->chunk_events));
+    }
+  }
+  c->ce_h = H;
+  return HFR_SUCCESS;
+}
+
 // CE schedule, chunk-pipelined (Alg. 1's "split Dg by Chunk_Size" + the
 // paper's pipelining): shard r is cut into K chunks
-// (K the same on every rank: a function of count and n only).
-//   reduce-scatter pulls: helper stream j copies chunk i of shard r from peer
-//     q into staging slot q, back to back for i = 0..K-1 (copy engines);
-//   fold: stream s folds chunk i (SMs, local, rank order) as soon as its n-1
-//     pulls landed, then publishes ce_done[r] = (e << 20) | (i + 1) at every
-//     peer with a fenced stream write;
-//   all-gather pulls: helper stream j' waits (stream memop) until peer q
-//     published chunk i of shard q and copies it into this rank's buffer.
+// (K the same on every rank: a function of count and n only).  For every rank
+// r this process drives (one, or all n for a virtual comm):
+//   reduce-scatter pulls: helper streams copy chunk i of shard r from every
+//     peer q into staging slot q, back to back for i = 0..K-1 (copy engines,
+//     one cudaMemcpyAsync per copy);
+//   fold: r's fold stream folds chunk i (SMs, local, rank order) as soon as
+//     its n-1 pulls landed, then publishes ce_done[r] = (e << 20) | (i + 1) at
+//     every peer with a fenced stream write;
+//   all-gather pulls: helper streams wait (stream memop) until peer q
+//     published chunk i of shard q and copy it into r's buffer.
 // So chunk i's all-gather overlaps chunk i+1's reduce-scatter pull and fold.
 // Entry/exit: ce_ready / ce_exit handshakes (no SM involved).
-hfr_status_t run_ce(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, cudaStream_t s) {
-  const int n = c->n, r = c->rank;
+hfr_status_t run_ce(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, cudaStream_t s, size_t area) {
+  HFR_TRY(ce_streams(c));
+  const int n = c->n, L = c->local, H = c->ce_h;
   const size_t esz = dtype_size(dt);
   uint64_t lo[kMaxRanks + 1];
   for (int g = 0; g < n; ++g) lo[g] = count * g / n / 256 * 256;
   lo[n] = count;
-  const size_t slot = round_up((count / n + 256) * esz, kAlign);
-  char* stage = stage_base(c, r);
+  const size_t slot = ce_slot_bytes(c, count, dt);
   const uint64_t e = ++c->ce_epoch;
   StreamValueFn wr = nullptr, wt = nullptr;
   HFR_TRY(stream_value_fns(&wr, &wt));
@@ -882,90 +909,128 @@ hfr_status_t run_ce(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_
   const uint64_t shard_bytes = count / n * esz;
   const int K = (int)std::max<uint64_t>(1, std::min<uint64_t>(kCeMaxChunks, shard_bytes / kCeMinChunkBytes));
   auto chunk = [&](int g, int i, uint64_t* b, uint64_t* len) {  // chunk i of shard g, elements
-    const uint64_t L = lo[g + 1] - lo[g];
-    const uint64_t C = (L + K - 1) / K / 256 * 256 + 256;
-    const uint64_t s0 = std::min<uint64_t>(L, (uint64_t)i * C), s1 = std::min<uint64_t>(L, (uint64_t)(i + 1) * C);
+    const uint64_t Lg = lo[g + 1] - lo[g];
+    const uint64_t C = (Lg + K - 1) / K / 256 * 256 + 256;
+    const uint64_t s0 = std::min<uint64_t>(Lg, (uint64_t)i * C), s1 = std::min<uint64_t>(Lg, (uint64_t)(i + 1) * C);
     *b = lo[g] + s0;
-    *len = (i == K - 1 ? L : s1) - s0;
+    *len = (i == K - 1 ? Lg : s1) - s0;
   };
+  auto rank_of = [&](int l) { return c->virt ? l : c->rank; };
+  auto helper = [&](int l, int q) {  // helper index of peer q for local rank l
+    const int r = rank_of(l);
+    return l * H + (H == 1 ? 0 : (q < r ? q : q - 1));
+  };
+  // fold streams: the call's stream (real) or one per virtual rank, forked from it
+  cudaStream_t fs[kMaxRanks];
+  if (c->virt) {
+    HFR_CU(cudaEventRecord(c->ce_join[0], s));
+    for (int l = 0; l < L; ++l) {
+      fs[l] = c->ce_fold[l];
+      HFR_CU(cudaStreamWaitEvent(fs[l], c->ce_join[0], 0));
+    }
+  } else {
+    fs[0] = s;
+  }
   // 1. every rank's buffer is ready ("wait for chunk-i transfer")
-  HFR_TRY(ce_handshake(c, s, offsetof(Pad, ce_ready), e));
-  HFR_CU(cudaEventRecord(c->ce_fork, s));
-  // 2. reduce-scatter transfers: all chunks, back to back, per peer
-  int j = 0;
-  for (int q = 0; q < n; ++q) {
-    if (q == r) continue;
-    HFR_CU(cudaStreamWaitEvent(c->helpers[j], c->ce_fork, 0));
+  HFR_TRY(ce_handshake(c, fs, offsetof(Pad, ce_ready), e));
+  // 2. reduce-scatter transfers: all chunks, back to back, per helper
+  for (int l = 0; l < L; ++l) {
+    const int r = rank_of(l);
+    char* stage = stage_base(c, r) + area;
+    HFR_CU(cudaEventRecord(c->ce_fork[l], fs[l]));
+    for (int j = 0; j < H; ++j) {
+      HFR_CU(cudaStreamWaitEvent(c->helpers[l * H + j], c->ce_fork[l], 0));
+      HFR_CU(cudaStreamWaitEvent(c->ag_helpers[l * H + j], c->ce_fork[l], 0));
+    }
     for (int i = 0; i < K; ++i) {
       uint64_t b, len;
       chunk(r, i, &b, &len);
-      if (len)
+      for (int q = 0; q < n; ++q) {
+        if (q == r || !len) continue;
         HFR_CU(cudaMemcpyAsync(stage + (size_t)q * slot + (b - lo[r]) * esz, bufs[q] + b * esz, len * esz,
-                               cudaMemcpyDeviceToDevice, c->helpers[j]));
-      HFR_CU(cudaEventRecord(c->chunk_events[(size_t)j * kCeMaxChunks + i], c->helpers[j]));
+                               cudaMemcpyDeviceToDevice, c->helpers[helper(l, q)]));
+      }
+      for (int j = 0; j < H; ++j)
+        HFR_CU(cudaEventRecord(c->chunk_events[(size_t)(l * H + j) * kCeMaxChunks + i], c->helpers[l * H + j]));
     }
-    ++j;
   }
-  for (int jj = 0; jj < n - 1; ++jj) HFR_CU(cudaStreamWaitEvent(c->ag_helpers[jj], c->ce_fork, 0));
   // 3./4. per chunk: fold (SMs, local, rank order) once its pulls landed and
   // publish it; then the all-gather pulls of chunk i, each gated on the
   // owner's flag.  Host submission order matters: streams may share a
   // hardware queue, so a blocking stream wait is only ever submitted AFTER
-  // everything any rank's flag depends on (the RS pulls, this chunk's fold
-  // and flag write) — no false dependency can then deadlock the ranks.
+  // everything any rank's flag depends on (the RS pulls, this chunk's folds
+  // and flag writes of every local rank) — no false dependency can then
+  // deadlock the ranks.
   for (int i = 0; i < K; ++i) {
-    for (int jj = 0; jj < n - 1; ++jj) HFR_CU(cudaStreamWaitEvent(s, c->chunk_events[(size_t)jj * kCeMaxChunks + i], 0));
-    uint64_t b, len;
-    chunk(r, i, &b, &len);
-    if (len) {
-      FoldArgs f{};
-      for (int q = 0; q < n; ++q)
-        f.src[q] = q == r ? bufs[r] + b * esz : stage + (size_t)q * slot + (b - lo[r]) * esz;
-      f.dst = bufs[r] + b * esz;
-      f.count = len;
-      f.scale = c->cfg.scale;
-      f.n = n;
-      const int ctas = (int)std::max<uint64_t>(
-          1, std::min<uint64_t>(c->cfg.max_ctas > 0 ? c->cfg.max_ctas : c->num_sms, (len / 4 + 511) / 512));
-      if (dt == HFR_BFLOAT16)
-        hfr_local_fold_kernel<BF16><<<ctas, 512, 0, s>>>(f);
-      else if (dt == HFR_FLOAT16)
-        hfr_local_fold_kernel<F16><<<ctas, 512, 0, s>>>(f);
-      else
-        hfr_local_fold_kernel<F32><<<ctas, 512, 0, s>>>(f);
-      cudaError_t err = cudaGetLastError();
-      if (err != cudaSuccess) {
-        note_cuda(err, "hfr_local_fold_kernel");
-        return HFR_ERR_CUDA;
+    for (int l = 0; l < L; ++l) {
+      const int r = rank_of(l);
+      char* stage = stage_base(c, r) + area;
+      for (int j = 0; j < H; ++j)
+        HFR_CU(cudaStreamWaitEvent(fs[l], c->chunk_events[(size_t)(l * H + j) * kCeMaxChunks + i], 0));
+      uint64_t b, len;
+      chunk(r, i, &b, &len);
+      if (len) {
+        FoldArgs f{};
+        for (int q = 0; q < n; ++q)
+          f.src[q] = q == r ? bufs[r] + b * esz : stage + (size_t)q * slot + (b - lo[r]) * esz;
+        f.dst = bufs[r] + b * esz;
+        f.count = len;
+        f.scale = c->cfg.scale;
+        f.n = n;
+        const int ctas = (int)std::max<uint64_t>(
+            1, std::min<uint64_t>(c->cfg.max_ctas > 0 ? c->cfg.max_ctas : c->num_sms / L, (len / 4 + 511) / 512));
+        if (dt == HFR_BFLOAT16)
+          hfr_local_fold_kernel<BF16><<<ctas, 512, 0, fs[l]>>>(f);
+        else if (dt == HFR_FLOAT16)
+          hfr_local_fold_kernel<F16><<<ctas, 512, 0, fs[l]>>>(f);
+        else
+          hfr_local_fold_kernel<F32><<<ctas, 512, 0, fs[l]>>>(f);
+        cudaError_t err = cudaGetLastError();
+        if (err != cudaSuccess) {
+          note_cuda(err, "hfr_local_fold_kernel");
+          return HFR_ERR_CUDA;
+        }
+        ++c->launches;
       }
-      ++c->launches;
+      for (int q = 0; q < n; ++q) {
+        if (q == r) continue;
+        const unsigned long long dst = (unsigned long long)(c->pad.base[q] + offsetof(Pad, ce_done) + 8 * (size_t)r);
+        if (wr(fs[l], dst, (e << 20) | (uint64_t)(i + 1), kWriteFenced) != 0) {
+          g_cuda_error = "cuStreamWriteValue64 on peer memory failed";
+          return HFR_ERR_CUDA;
+        }
+      }
     }
-    for (int q = 0; q < n; ++q) {
-      if (q == r) continue;
-      const unsigned long long dst = (unsigned long long)(c->pad.base[q] + offsetof(Pad, ce_done) + 8 * (size_t)r);
-      if (wr(s, dst, (e << 20) | (uint64_t)(i + 1), kWriteFenced) != 0) {
-        g_cuda_error = "cuStreamWriteValue64 on peer memory failed";
-        return HFR_ERR_CUDA;
+    for (int l = 0; l < L; ++l) {
+      const int r = rank_of(l);
+      for (int q = 0; q < n; ++q) {
+        if (q == r) continue;
+        cudaStream_t h = c->ag_helpers[helper(l, q)];
+        const unsigned long long flag = (unsigned long long)(c->pad.base[r] + offsetof(Pad, ce_done) + 8 * (size_t)q);
+        if (wt(h, flag, (e << 20) | (uint64_t)(i + 1), kWaitGeq) != 0) {
+          g_cuda_error = "cuStreamWaitValue64 failed";
+          return HFR_ERR_CUDA;
+        }
+        uint64_t qb, qlen;
+        chunk(q, i, &qb, &qlen);
+        if (qlen) HFR_CU(cudaMemcpyAsync(bufs[r] + qb * esz, bufs[q] + qb * esz, qlen * esz, cudaMemcpyDeviceToDevice, h));
       }
-    }
-    int jq = 0;
-    for (int q = 0; q < n; ++q) {
-      if (q == r) continue;
-      cudaStream_t h = c->ag_helpers[jq++];
-      const unsigned long long flag = (unsigned long long)(c->pad.base[r] + offsetof(Pad, ce_done) + 8 * (size_t)q);
-      if (wt(h, flag, (e << 20) | (uint64_t)(i + 1), kWaitGeq) != 0) {
-        g_cuda_error = "cuStreamWaitValue64 failed";
-        return HFR_ERR_CUDA;
-      }
-      uint64_t qb, qlen;
-      chunk(q, i, &qb, &qlen);
-      if (qlen) HFR_CU(cudaMemcpyAsync(bufs[r] + qb * esz, bufs[q] + qb * esz, qlen * esz, cudaMemcpyDeviceToDevice, h));
     }
   }
-  for (int jj = 0; jj < n - 1; ++jj) HFR_CU(cudaEventRecord(c->ag_events[jj], c->ag_helpers[jj]));
-  for (int jj = 0; jj < n - 1; ++jj) HFR_CU(cudaStreamWaitEvent(s, c->ag_events[jj], 0));
+  for (int l = 0; l < L; ++l)
+    for (int j = 0; j < H; ++j) {
+      HFR_CU(cudaEventRecord(c->ag_events[l * H + j], c->ag_helpers[l * H + j]));
+      HFR_CU(cudaStreamWaitEvent(fs[l], c->ag_events[l * H + j], 0));
+    }
   // 5. every rank finished pulling from every buffer
-  return ce_handshake(c, s, offsetof(Pad, ce_exit), e);
+  HFR_TRY(ce_handshake(c, fs, offsetof(Pad, ce_exit), e));
+  if (c->virt) {
+    for (int l = 0; l < L; ++l) {
+      HFR_CU(cudaEventRecord(c->ce_join[l], fs[l]));
+      HFR_CU(cudaStreamWaitEvent(s, c->ce_join[l], 0));
+    }
+  }
+  return HFR_SUCCESS;
 }
 
 hfr_status_t run_nvls(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig, uint64_t offset,
@@ -1058,8 +1123,19 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   HFR_CU(cudaStreamIsCapturing(user, &cap));
   const bool capturing = cap != cudaStreamCaptureStatusNone;
-  if (capturing && count > 0 && scratch_need(c, count, dt, algo) > c->scratch.bytes)
-    return HFR_ERR_UNSUPPORTED;  // scratch growth is collective and synchronous: call once before capturing
+  const size_t esz = dtype_size(dt);
+  const size_t bytes = count * esz;
+  // zero-copy iff every local buffer is 16-B aligned and (real comm) lies in
+  // peer-mapped memory; otherwise stage through the scratch.
+  bool aligned = true;
+  for (int q = 0; q < c->local; ++q) aligned &= (reinterpret_cast<uintptr_t>(local_bufs[q]) & 15) == 0;
+  const Region* reg = nullptr;
+  const bool zero_copy = count > 0 && aligned && (c->virt || find_region(c, local_bufs[0], bytes, &reg));
+  const uint64_t offset = zero_copy && reg ? (uint64_t)(local_bufs[0] - reg->base[c->rank]) : 0;
+  // ONESHOT never stages (peers never touch this rank's buffer)
+  const size_t need = count == 0 ? 0 : scratch_need(c, count, dt, algo, zero_copy || algo == HFR_ALGO_ONESHOT);
+  if (capturing && need > c->scratch.bytes)
+    return HFR_ERR_UNSUPPORTED;  // scratch growth is collective: call once before capturing
   // the CE schedule's stream-memop flags carry a host-side epoch, which a
   // replayed graph would repeat (stale flags would pass): not capturable
   if (capturing && count > 0 && algo == HFR_ALGO_CE) return HFR_ERR_UNSUPPORTED;
@@ -1072,24 +1148,12 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     HFR_CU(cudaStreamWaitEvent(c->side, ready, 0));
     c->ev_pool.push_back(ready);
     s = c->side;
-  } else if (c->side_busy && !capturing) {
-    // keep every call of this comm in issue order: the caller's stream waits
-    // for the asynchronous calls issued before this one
-    HFR_CU(cudaEventRecord(c->side_tail, c->side));
-    HFR_CU(cudaStreamWaitEvent(user, c->side_tail, 0));
-    c->side_busy = false;
   }
+  // issue order: after the previous call of this comm, whatever its stream
+  // (captured calls are ordered by their capture stream alone)
+  if (!capturing && c->has_last) HFR_CU(cudaStreamWaitEvent(s, c->last_op, 0));
   if (count > 0) {
-    const size_t esz = dtype_size(dt);
-    const size_t bytes = count * esz;
-    // zero-copy iff every local buffer is 16-B aligned and (real comm) lies in
-    // peer-mapped memory; otherwise stage through the scratch.
-    bool aligned = true;
-    for (int q = 0; q < c->local; ++q) aligned &= (reinterpret_cast<uintptr_t>(local_bufs[q]) & 15) == 0;
-    const Region* reg = nullptr;
-    bool zero_copy = aligned && (c->virt || find_region(c, local_bufs[0], bytes, &reg));
-    uint64_t offset = zero_copy && reg ? (uint64_t)(local_bufs[0] - reg->base[c->rank]) : 0;
-    HFR_TRY(ensure_scratch(c, scratch_need(c, count, dt, algo)));
+    HFR_TRY(ensure_scratch(c, need));
     uint64_t sig = 1469598103934665603ull;
     sig = fnv(sig, count);
     sig = fnv(sig, (uint64_t)dt | ((uint64_t)op << 8) | ((uint64_t)algo << 16) | ((uint64_t)coll << 24) |
@@ -1098,7 +1162,7 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     memcpy(&sbits, &c->cfg.scale, 4);
     sig = fnv(sig, sbits);
     const bool gate = c->cfg.stream_gate && !c->virt && c->n > 1 && algo != HFR_ALGO_CE && !capturing;
-    if (gate) HFR_TRY(ce_handshake(c, s, offsetof(Pad, ce_ready), ++c->ce_epoch));
+    if (gate) HFR_TRY(ce_handshake(c, &s, offsetof(Pad, ce_ready), ++c->ce_epoch));
     if (algo == HFR_ALGO_ONESHOT) {
       // peers never touch this rank's buffer: no staging, any device pointer
       HFR_TRY(run_oneshot(c, local_bufs, count, dt, sig, s));
@@ -1115,18 +1179,19 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
         HFR_TRY(run_copy(c, stage_base(c, r), local_bufs[q], bytes, s));
       }
     }
+    const size_t area = msg_stage_bytes(count, dt, zero_copy);  // the schedule's scratch area
     sig = fnv(sig, (uint64_t)zero_copy);
     sig = fnv(sig, algo == HFR_ALGO_FLAT ? 0 : tree_chunk(c));
     sig = fnv(sig, offset);
     if (algo == HFR_ALGO_NVLS) {
       if (!zero_copy || !reg || !reg->nvls || !c->nvls || !c->nvls->on) return HFR_ERR_UNSUPPORTED;
       HFR_TRY(run_nvls(c, bufs, count, dt, sig, offset, s, coll, root));
-    } else if (algo == HFR_ALGO_CE && zero_copy) {
-      HFR_TRY(run_ce(c, bufs, count, dt, s));
-    } else if (algo == HFR_ALGO_FLAT || algo == HFR_ALGO_CE) {
-      HFR_TRY(run_flat(c, bufs, count, dt, sig, s, coll, root, zero_copy ? reg : nullptr, offset));
+    } else if (algo == HFR_ALGO_CE) {
+      HFR_TRY(run_ce(c, bufs, count, dt, s, area));
+    } else if (algo == HFR_ALGO_FLAT) {
+      HFR_TRY(run_flat(c, bufs, count, dt, sig, s, coll, root));
     } else {
-      HFR_TRY(run_tree(c, bufs, count, dt, algo == HFR_ALGO_PAIR_DBT, sig, s));
+      HFR_TRY(run_tree(c, bufs, count, dt, algo == HFR_ALGO_PAIR_DBT, sig, s, area));
     }
     if (!zero_copy) {
       for (int q = 0; q < c->local; ++q) {
@@ -1137,8 +1202,11 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
     }
   }
 done:
+  if (!capturing) {
+    HFR_CU(cudaEventRecord(c->last_op, s));
+    c->has_last = true;
+  }
   if (req) {
-    c->side_busy = true;
     cudaEvent_t done = take_event(c);
     if (!done) return HFR_ERR_CUDA;
     HFR_CU(cudaEventRecord(done, s));
@@ -1384,9 +1452,19 @@ hfr_status_t hfr_barrier(hfr_comm_t c, hfr_stream_t stream) {
   if (!c) return HFR_ERR_NOT_INITIALIZED;
   if (c->sticky != HFR_SUCCESS) return c->sticky;
   DeviceGuard guard(c->dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  HFR_CU(cudaStreamIsCapturing(s, &cap));
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  if (!capturing && c->has_last) HFR_CU(cudaStreamWaitEvent(s, c->last_op, 0));  // issue order
   Args a;
   base_args(c, a, 0, 0xBA881E8ull);
-  return launch(c, (const void*)hfr_barrier_kernel, 1, 32 * ((c->n + 31) / 32), a, (cudaStream_t)stream, true);
+  HFR_TRY(launch(c, (const void*)hfr_barrier_kernel, 1, 32 * ((c->n + 31) / 32), a, s, true));
+  if (!capturing) {
+    HFR_CU(cudaEventRecord(c->last_op, s));
+    c->has_last = true;
+  }
+  return HFR_SUCCESS;
 }
 
 hfr_status_t hfr_finalize(hfr_comm_t c) {
@@ -1401,6 +1479,8 @@ hfr_status_t hfr_finalize(hfr_comm_t c) {
     }
     for (Region& r : c->regions) close_region(c, r);
     c->regions.clear();
+    for (Region& r : c->retired) close_region(c, r);
+    c->retired.clear();
     close_region(c, c->scratch);
     close_region(c, c->pad);
     if (c->nvls) {
@@ -1408,12 +1488,15 @@ hfr_status_t hfr_finalize(hfr_comm_t c) {
       delete c->nvls;
     }
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    for (cudaStream_t h : c->ce_fold) cudaStreamDestroy(h);
     for (cudaStream_t h : c->helpers) cudaStreamDestroy(h);
     for (cudaStream_t h : c->ag_helpers) cudaStreamDestroy(h);
     for (cudaEvent_t e : c->ag_events) cudaEventDestroy(e);
     for (cudaEvent_t e : c->chunk_events) cudaEventDestroy(e);
-    if (c->ce_fork) cudaEventDestroy(c->ce_fork);
-    if (c->side_tail) cudaEventDestroy(c->side_tail);
+    for (cudaEvent_t e : c->ce_fork) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ce_join) cudaEventDestroy(e);
+    if (c->last_op) cudaEventDestroy(c->last_op);
+    if (c->setup) cudaStreamDestroy(c->setup);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->err_host) cudaFreeHost(c->err_host);
   }

@@ -14,18 +14,32 @@ compute stream, so the reduction overlaps the rest of the backward.  finish()
 orders every bucket's completion back onto the compute stream before the
 optimizer step.  The comm kernels are capped at `max_ctas` CTAs so they leave
 most SMs to the backward GEMMs (unlike the paper's copy-engine HFReduce,
-PAPER.md:375, an SM-driven allreduce is not free — DESIGN.md §6).
+PAPER.md:375, an SM-driven allreduce is not free — DESIGN.md §6); algo "ce"
+moves the bytes with the copy engines instead (only a local fold on the SMs).
+
+A virtual comm (n ranks on one GPU, hfr_init_virtual) gets one arena per
+virtual rank and reduces each bucket across them with one
+hfr_allreduce_virtual: the same kernels and bucket plan as one rank per GPU,
+so the bucketed path is parity-tested on a single B200.
+
+Configs.  `config` (the overlapped buckets) and `tail_config` (the buckets
+completed by the last gradient GEMM, with nothing left to hide behind) are
+full hfr configs; build them from the comm's own with
+`HaiScaleDDP.derive(comm, max_ctas=..., ...)` (= dataclasses.replace of
+comm.config) so the gradient scale carries over.  A config whose scale
+differs from the comm's raises instead of silently summing where the caller
+averages.  finish() restores the comm's config.
 
 Measured on 4 B200s with a 7e9-parameter LLaMA-shaped backward (C5, median
 of 15 interleaved repetitions): the best bit-exact setting is FLAT with
-Config(max_ctas=32..40, threads=128, stream_gate=1, flat_staging=1) — small
-register-staged comm CTAs (no shared memory) share SMs with the GEMM CTAs —
-plus a full-width tail_config for the buckets completed by the last gradient
-GEMM, for an overlap of 0.90-0.95 over runs (0.91 without the tail); algo "nvls"
-(order-relaxed) with 16 CTAs reaches 0.98-0.99.
+derive(comm, max_ctas=32..40, threads=128, stream_gate=1, flat_staging=1) —
+small register-staged comm CTAs (no shared memory) share SMs with the GEMM
+CTAs — plus a full-width tail_config, for an overlap of 0.90-0.95 over runs;
+algo "nvls" (order-relaxed) with 16 CTAs reaches 0.98-0.99.
 """
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 from typing import List, Optional, Sequence, Tuple
 
@@ -67,13 +81,21 @@ class BucketStats:
 
 
 class HaiScaleDDP:
-    """Gradient arena + asynchronous bucketed allreduce for one rank.
+    """Gradient arena + asynchronous bucketed allreduce for one rank (or all
+    virtual ranks of a virtual comm).
 
     Usage per step:
         ddp.zero_grad()                     (optional; the backward may overwrite instead)
         for i in backward order: write ddp.grad(i); ddp.mark_ready(i, stream)
         ddp.finish(stream)                  (stream waits for every bucket)
+    grad(i) / bucket(k) are tensors for a real comm and lists of tensors (one
+    per virtual rank) for a virtual comm.
     """
+
+    @staticmethod
+    def derive(comm, **changes):
+        """comm.config with `changes` applied (keeps scale, timeout, ...)."""
+        return dataclasses.replace(comm.config, **changes)
 
     def __init__(self, comm, numels: Sequence[int], dtype, bucket_bytes: int = 64 << 20,
                  config=None, tail_config=None, tail_from: Optional[int] = None):
@@ -82,14 +104,16 @@ class HaiScaleDDP:
         completed by marking parameter `tail_from` (backward order) or a later
         one — the last gradient GEMM of the step; nothing is left to overlap
         them with, so they may take the whole GPU.  tail_from None: the last
-        parameter.  tail_config None: `config` throughout; both None: the
-        comm's current config; tail_config without config: ValueError.
-        Every rank makes the same choice for the same bucket (collective
-        contract, include/hfr.h)."""
+        parameter.  None configs: the comm's config.  Every rank makes the
+        same choice for the same bucket (collective contract, include/hfr.h)."""
         import torch
-        if tail_config is not None and config is None:
-            raise ValueError("tail_config needs config (the comm's config is not restored otherwise)")
+        base = comm.config
+        for name, cfg in (("config", config), ("tail_config", tail_config)):
+            if cfg is not None and cfg.scale != base.scale:
+                raise ValueError(f"{name}.scale={cfg.scale} differs from the comm's scale {base.scale}: build it "
+                                 "with HaiScaleDDP.derive(comm, ...) (or set the comm's scale first)")
         self.comm = comm
+        self.base = base
         self.config = config
         self.tail_config = tail_config
         self.tail_from = len(numels) - 1 if tail_from is None else tail_from
@@ -98,9 +122,10 @@ class HaiScaleDDP:
         self.bucket_elems = max(1, bucket_bytes // esz)
         self.param_ranges, self.bucket_ranges, self.bucket_params = plan_buckets(list(numels), self.bucket_elems)
         self.total = self.param_ranges[-1][1] if self.param_ranges else 0
-        self.arena = comm.empty(max(1, self.total), dtype)
-        if isinstance(self.arena, list):
-            raise ValueError("HaiScaleDDP needs a real (one rank per process) comm")
+        arena = comm.empty(max(1, self.total), dtype)
+        self.virtual = isinstance(arena, list)
+        self.arenas = arena if self.virtual else [arena]
+        self.arena = arena
         self._pending = [len(m) for m in self.bucket_params]
         self._active = None
         self._bucket_of_param: List[List[int]] = [[] for _ in numels]
@@ -111,15 +136,18 @@ class HaiScaleDDP:
         self.stats = BucketStats()
 
     def zero_grad(self):
-        self.arena.zero_()
+        for a in self.arenas:
+            a.zero_()
+
+    def _view(self, s: int, e: int):
+        views = [a[s:e] for a in self.arenas]
+        return views if self.virtual else views[0]
 
     def grad(self, i: int):
-        s, e = self.param_ranges[i]
-        return self.arena[s:e]
+        return self._view(*self.param_ranges[i])
 
     def bucket(self, k: int):
-        s, e = self.bucket_ranges[k]
-        return self.arena[s:e]
+        return self._view(*self.bucket_ranges[k])
 
     def reset(self):
         self._pending = [len(m) for m in self.bucket_params]
@@ -127,7 +155,8 @@ class HaiScaleDDP:
         self._active = None  # re-apply the configs each step (the caller may have changed the comm's)
 
     def _use(self, cfg):
-        if cfg is not None and cfg is not self._active:
+        cfg = cfg if cfg is not None else self.base
+        if cfg is not self._active:
             self.comm.set_config(cfg)
             self._active = cfg
 
@@ -139,21 +168,31 @@ class HaiScaleDDP:
         for k in self._bucket_of_param[i]:
             self._pending[k] -= 1
             if self._pending[k] == 0:
-                self._use(self.tail_config if tail else self.config)
+                if self.config is not None or self.tail_config is not None:
+                    self._use(self.tail_config if tail else self.config)
                 self.stats.tail += int(tail)
                 self._launch(k, stream)
 
     def _launch(self, k: int, stream):
         b = self.bucket(k)
-        self._works.append(self.comm.allreduce(b, async_op=True, stream=stream))
+        if self.virtual:
+            w = self.comm.allreduce_virtual(b, async_op=True, stream=stream)
+            nbytes = b[0].numel() * b[0].element_size()
+        else:
+            w = self.comm.allreduce(b, async_op=True, stream=stream)
+            nbytes = b.numel() * b.element_size()
+        self._works.append(w)
         self.stats.launched += 1
-        self.stats.bytes += b.numel() * b.element_size()
+        self.stats.bytes += nbytes
 
     def finish(self, stream=None):
-        """Make `stream` wait for every launched bucket (no host block)."""
+        """Make `stream` wait for every launched bucket (no host block) and
+        restore the comm's own config."""
         for w in self._works:
             w.wait(stream=stream)
         self._works = []
         if any(p != 0 for p in self._pending):
             raise RuntimeError("finish() before every gradient was marked ready")
+        if self._active is not None and self._active is not self.base:
+            self.comm.set_config(self.base)
         self.reset()

@@ -159,6 +159,26 @@ def gpu_cases(rank, world, port, outdir):
             else:
                 res["fail"].append(f"protocol: got {e}")
         comm.finalize()
+        # argument mismatches that change the grid (4096 vs 4 Mi elements) or
+        # even the kernel (AUTO: LL ONESHOT on one rank, FLAT on the other):
+        # PROTOCOL within a fraction of the timeout, never TIMEOUT
+        import time
+        for algo in ("flat", "auto"):
+            pc = hfr.Comm.init(device=rank, config=hfr.Config(algo=algo, timeout_ms=20000))
+            t = pc.empty(4 << 20, torch.float32)
+            cnt = 4096 if rank % 2 == 0 else (4 << 20)
+            t0 = time.time()
+            try:
+                pc.allreduce(t[:cnt], async_op=True).wait(host=True)
+                res["fail"].append(f"protocol-{algo}: mismatch not detected")
+            except hfr.HfrError as e:
+                dt_s = time.time() - t0
+                if e.status == hfr.ERR_PROTOCOL and dt_s < 10:
+                    res["ok"].append(f"protocol-grid-{algo}")
+                else:
+                    res["fail"].append(f"protocol-{algo}: got {e} after {dt_s:.1f} s")
+            dist.barrier()
+            pc.finalize()
         # NVLS order-relaxed path (reading R18 bound), if the box has multicast
         comm = hfr.Comm.init(device=rank, config=hfr.Config(timeout_ms=8000, nvls_bytes=64 << 20, algo="nvls",
                                                             scale=0.5))

@@ -53,18 +53,20 @@ def test_bad_bucket():
 class _FakeComm:
     """Records (config, bucket offset) per allreduce; CPU tensors only."""
 
-    def __init__(self):
-        self.cfg, self.calls = None, []
+    def __init__(self, scale=1.0):
+        from paper_2408_14158_b200 import Config
+        self.config = Config(scale=scale)
+        self.calls = []
 
     def empty(self, numel, dtype):
         import torch
         return torch.zeros(numel, dtype=dtype)
 
     def set_config(self, cfg):
-        self.cfg = cfg
+        self.config = cfg
 
     def allreduce(self, t, async_op=False, stream=None):
-        self.calls.append((self.cfg, t.data_ptr()))
+        self.calls.append((self.config, t.data_ptr()))
 
         class _W:
             def wait(self, stream=None):
@@ -77,21 +79,26 @@ def test_tail_config_covers_exactly_the_late_buckets(tail_from):
     import torch
     from paper_2408_14158_b200.ddp import HaiScaleDDP
     numels = [40, 17, 100, 3, 60]
-    comm = _FakeComm()
-    ddp = HaiScaleDDP(comm, numels, torch.float32, bucket_bytes=16 * 4, config="overlap", tail_config="tail",
+    comm = _FakeComm(scale=0.25)
+    overlap = HaiScaleDDP.derive(comm, max_ctas=8)
+    tail = HaiScaleDDP.derive(comm, max_ctas=0, algo="flat")
+    ddp = HaiScaleDDP(comm, numels, torch.float32, bucket_bytes=16 * 4, config=overlap, tail_config=tail,
                       tail_from=tail_from)
+    base = comm.config
     tf = len(numels) - 1 if tail_from is None else tail_from
     for step in range(2):
         comm.calls = []
         for i in range(len(numels)):
             ddp.mark_ready(i)
         ddp.finish()
+        assert comm.config is base, "finish() restores the comm's config"
         assert len(comm.calls) == len(ddp.bucket_ranges)
         esz = 4
         for cfg, ptr in comm.calls:
             k = (ptr - ddp.arena.data_ptr()) // esz // ddp.bucket_elems
             last_member = max(ddp.bucket_params[k])
-            assert cfg == ("tail" if last_member >= tf else "overlap"), (k, cfg)
+            assert cfg is (tail if last_member >= tf else overlap), (k, cfg)
+            assert cfg.scale == 0.25
     assert ddp.stats.tail == 2 * sum(1 for m in ddp.bucket_params if max(m) >= tf)
 
 
@@ -99,11 +106,12 @@ def test_no_configs_leaves_comm_config_alone():
     import torch
     from paper_2408_14158_b200.ddp import HaiScaleDDP
     comm = _FakeComm()
+    base = comm.config
     ddp = HaiScaleDDP(comm, [10, 20], torch.float32, bucket_bytes=32)
     for i in range(2):
         ddp.mark_ready(i)
     ddp.finish()
-    assert all(c is None for c, _ in comm.calls) and ddp.stats.tail == 0
+    assert all(c is base for c, _ in comm.calls) and ddp.stats.tail == 0
 
 
 def test_c5_tail_buckets_are_the_embedding_gemm_buckets():
@@ -119,8 +127,16 @@ def test_c5_tail_buckets_are_the_embedding_gemm_buckets():
     assert 7 * (64 << 20) // 2 < params[tail_from][1] * params[tail_from][2] < 8 * (64 << 20) // 2  # 7.8 buckets over 9
 
 
-def test_tail_config_requires_config():
+def test_config_scale_must_match_the_comm():
+    """a DDP config built from scratch (scale 1.0) on a comm that
+    averages (scale 1/n) would silently sum — refused."""
     import torch
+    from paper_2408_14158_b200 import Config
     from paper_2408_14158_b200.ddp import HaiScaleDDP
+    comm = _FakeComm(scale=0.125)
     with pytest.raises(ValueError):
-        HaiScaleDDP(_FakeComm(), [10, 20], torch.float32, bucket_bytes=32, tail_config="tail")
+        HaiScaleDDP(comm, [10, 20], torch.float32, bucket_bytes=32, config=Config(max_ctas=32))
+    with pytest.raises(ValueError):
+        HaiScaleDDP(comm, [10, 20], torch.float32, bucket_bytes=32, tail_config=Config())
+    ddp = HaiScaleDDP(comm, [10, 20], torch.float32, bucket_bytes=32, tail_config=HaiScaleDDP.derive(comm))
+    assert ddp.tail_config.scale == 0.125

@@ -32,4 +32,5 @@ def test_multiprocess_parity_protocol_timeout(tmp_path):
         res = json.load(open(os.path.join(tmp_path, f"rank{r}.json")))
         assert not res["fail"], res["fail"]
         assert "protocol" in res["ok"] and "ddp" in res["ok"] and "1gib" in res["ok"] and "ddp-tail-1" in res["ok"]
+        assert "protocol-grid-flat" in res["ok"] and "protocol-grid-auto" in res["ok"]
         assert len(res["ok"]) >= 10
