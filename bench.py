@@ -14,9 +14,14 @@ memory (zero-copy), scale = 1/n (gradient averaging, fused into the epilogue).
          protocol with HBM as the transport ("C2-virtual8").
   N > 1  one rank per GPU over NVLink/NVSwitch ("C2-nvlink"), n = N.
 
-A step is one allreduce of the whole buffer.  value = busBW = S/t * 2(n-1)/n
-(nccl-tests convention, reading R15) with t the per-step device time, max over
-ranks; inputs (186 MiB per rank) exceed the 126 MB L2, so no flush is needed.
+A step is one allreduce of the whole buffer, t its device time (max over
+ranks); inputs (186 MiB per rank) exceed the 126 MB L2, so no flush is needed.
+  N > 1  value = busBW = S/t * 2(n-1)/n (nccl-tests convention, reading R15),
+         roofline against the per-direction NVLink peak MEASURED on this lease
+         (tools/p2p_probe.cu, all GPUs moving at once) and against 900 nominal.
+  N = 1  busBW is 0 for one GPU: value = algBW = S/t of the 8
+         virtual-rank allreduce, roofline against the measured HBM bandwidth
+         (2·n·S bytes per launch); the 8-rank busBW is kept as `busbw_virtual`.
 """
 from __future__ import annotations
 
@@ -32,7 +37,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "allreduce bus GB/s (max over ranks) at 2/4/8 B200 vs NCCL & 900 GB/s NVLink"
-NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction (900 nominal)
+NVLINK_GUIDE_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (fallback only)
 NVLINK_NOMINAL_GBS = 900.0
 
 
@@ -72,6 +77,12 @@ def busbw(bytes_per_rank: float, seconds: float, n: int) -> float:
 
 def algbw(bytes_per_rank: float, seconds: float) -> float:
     return bytes_per_rank / seconds / 1e9
+
+
+def headline(bytes_per_rank: float, seconds: float, n: int, multi: bool) -> float:
+    """The line's `value`: busBW over NVLink (N > 1); algBW of the virtual-rank
+    allreduce on one GPU (N = 1, where busBW is 0 by definition)."""
+    return busbw(bytes_per_rank, seconds, n) if multi else algbw(bytes_per_rank, seconds)
 
 
 # ---------------------------------------------------------------------------
@@ -127,10 +138,23 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # CPU baseline: the C oracle (oracle/fold.c) on the host cores
 # ---------------------------------------------------------------------------
-def cpu_oracle_run(n: int, count: int, dtype: str, budget_s: float, max_reps: int = 1000):
+def host_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def cpu_oracle_run(n: int, count: int, dtype: str, budget_s: float, max_reps: int = 1000, threads: int = 0):
     import hfr_inputs as gen
     from oracle import cfold
     xs = gen.rank_inputs(n, count, dtype, "grad", seed_base=1000)
+    cfold.set_threads(threads if threads > 0 else (os.cpu_count() or 1))
     cfold.fold_ascending(xs, 1.0 / n)  # warm (page in)
     times = []
     t_end = time.perf_counter() + budget_s
@@ -138,7 +162,30 @@ def cpu_oracle_run(n: int, count: int, dtype: str, budget_s: float, max_reps: in
         t0 = time.perf_counter()
         cfold.fold_ascending(xs, 1.0 / n)
         times.append(time.perf_counter() - t0)
-    return times, cfold.threads()
+    used = cfold.threads()
+    cfold.set_threads(os.cpu_count() or 1)
+    return times, used
+
+
+def cpu_baseline(n: int, count: int, dtype: str, esz: int, multi: bool, budget_s: float = 10.0):
+    """The oracle (oracle/fold.c, rank-ascending fold, as it stands) on the
+    host cores: all cores on the full workload (n x count), plus one thread
+    on a 1/16 sample; the line's own metric (busBW-equivalent
+    at N > 1, algBW at N = 1), as if the CPU fold were the allreduce."""
+    S = count * esz
+    times, cores = cpu_oracle_run(n, count, dtype, budget_s=budget_s)
+    tc = statistics.median(times)
+    small = max(4096, count // 16)
+    t1, _ = cpu_oracle_run(n, small, dtype, budget_s=budget_s / 2, max_reps=50, threads=1)
+    t1m = statistics.median(t1)
+    def metric(b, t):
+        return headline(b, t, n, multi)
+    return {"value": metric(S, tc), "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "sample": f"full workload ({n} x {count} {dtype}), oracle/fold.c rank-ascending fold, median of "
+                      f"{len(times)} reps (~{budget_s:.0f} s), {'busBW' if multi else 'algBW'}-equivalent",
+            "one_thread": {"value": metric(small * esz, t1m), "unit": "GB/s", "cores": 1,
+                           "sample": f"{n} x {small} {dtype} (1/16 of the workload), median of {len(t1)} reps"},
+            "host": host_info()}
 
 
 def reference_arm(args):
@@ -162,19 +209,29 @@ def reference_arm(args):
     for _ in range(args.steps):
         cfold.fold_ascending(xs, 1.0 / n)
     t = (time.perf_counter() - t0) / args.steps
-    v = busbw(S, t, n)
+    multi = args.gpus > 1
+    v = headline(S, t, n, multi)
     cores = cfold.threads()
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+        "value_definition": value_definition(multi),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
         "config": workload_config(args, n, count, dtype),
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle",
                          "sample": f"full workload: rank-ascending fold of {n} x {count} {dtype} elements per step "
-                                   f"(oracle/fold.c, OpenMP {cores} threads), busBW-equivalent S/t*2(n-1)/n"},
+                                   f"(oracle/fold.c, OpenMP {cores} threads), "
+                                   f"{'busBW' if multi else 'algBW'}-equivalent", "host": host_info()},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def value_definition(multi: bool) -> str:
+    if multi:
+        return "busBW = S/t*2(n-1)/n, t = device time per allreduce, max over ranks (nccl-tests convention)"
+    return ("algBW = S/t of the 8-virtual-rank allreduce on one B200 (busBW is 0 for one GPU, SURVEY §8(d)); "
+            "the virtual-rank busBW is busbw_virtual")
 
 
 def workload_config(args, n, count, dtype):
@@ -189,6 +246,102 @@ def workload_config(args, n, count, dtype):
         "l2": "inputs larger than L2 (bytes_per_rank > 126 MB), no flush",
         "parallelism": f"dp{args.gpus}",
     }
+
+
+# ---------------------------------------------------------------------------
+# NVLink per-direction peak measured on this lease (the roofline
+# denominator must not be a number copied from a guide)
+# ---------------------------------------------------------------------------
+PROBE_SRC = os.path.join(ROOT, "tools", "p2p_probe.cu")
+PROBE_BIN = os.path.join(ROOT, "tools", "p2p_probe")
+
+
+def nvlink_probe(n: int):
+    """Run tools/p2p_probe.cu over GPUs 0..n-1 (all moving at once, 256 MiB per
+    peer, 148 CTAs x 512 threads) and return {pattern: GB/s per GPU per
+    direction}; None if it cannot run."""
+    import re
+    try:
+        if not os.path.exists(PROBE_BIN) or os.path.getmtime(PROBE_BIN) < os.path.getmtime(PROBE_SRC):
+            subprocess.run(["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                            "-o", PROBE_BIN, PROBE_SRC], check=True, capture_output=True, timeout=300)
+        out = subprocess.run([PROBE_BIN, str(n), "256", "148", "512"], check=True, capture_output=True,
+                             text=True, timeout=300).stdout
+    except (OSError, subprocess.SubprocessError):
+        return None
+    res = {}
+    for line in out.splitlines():
+        m = re.match(r"n=\d+ (.+?)\s+\d+ MiB/peer.*->\s+([\d.]+) GB/s", line)
+        if m:
+            res[m.group(1).strip()] = float(m.group(2))
+    return res or None
+
+
+def nvlink_peak(probe):
+    """The roofline denominator: the best all-GPUs-at-once pattern (pull,
+    push or mixed pull/push — FLAT's own traffic is the mixed one)."""
+    if not probe:
+        return NVLINK_GUIDE_GBS, "fallback: B200_PROFILING.md peer copy 770 GB/s/dir (probe unavailable)"
+    keys = [k for k in probe if k.startswith(("read  (pull", "write (push", "mixed"))]
+    if not keys:
+        return NVLINK_GUIDE_GBS, "fallback: B200_PROFILING.md peer copy 770 GB/s/dir (probe parse failed)"
+    best = max(keys, key=lambda k: probe[k])
+    return probe[best], f"measured on this lease: tools/p2p_probe.cu '{best}', all {len(keys)} all-GPU patterns"
+
+
+def source_sha():
+    """sha256 of the library sources (the .so itself embeds box-local paths)."""
+    import hashlib
+    from paper_2408_14158_b200 import _build
+    h = hashlib.sha256()
+    for p in _build.DEPS:
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
+def committed_traffic(key: str):
+    """ncu DRAM (+ NVLink) bytes per launch for this kernel/config from
+    profiles/traffic.json, only if captured from the current sources."""
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        rec = json.load(open(prof)).get(key)
+    except (OSError, ValueError):
+        return None, None
+    if not isinstance(rec, dict):
+        return None, None
+    if rec.get("source_sha") != source_sha():
+        return None, {"stale": rec.get("source"), "captured_sha": rec.get("source_sha"), "current_sha": source_sha()}
+    return rec, {"source": rec.get("source"), "source_sha": rec.get("source_sha")}
+
+
+def variant_dir_bytes(hfr, algo: str, n: int, S: int, esz: int) -> float:
+    """Algorithmic NVLink bytes per direction of the busiest rank for one
+    allreduce of S bytes per rank, from the trees the
+    library builds (hfr_tree_query): up-pass partials fp32 (16-bit DBT leaves
+    send raw 16-bit values), down pass in the buffer dtype; PAIR adds the pair
+    reduce-scatter and all-gather halves; NVLS (n+1)/n·S."""
+    if algo == "nvls":
+        return (n + 1) / n * S
+    N = S / esz
+    pair = algo == "pair_dbt"
+    m = n // 2 if pair else n
+    data = N / 2 if pair else N             # elements each tree set covers
+    eg = [0.0] * m
+    ing = [0.0] * m
+    for which in (0, 1):                    # half of the chunks ride each tree
+        parent, children = hfr.tree_query(m, which)
+        for v in range(m):
+            for c in children[v]:
+                up = (esz if (not pair and esz == 2 and not children[c]) else 4) * data / 2
+                eg[c] += up
+                ing[v] += up
+                eg[v] += esz * data / 2     # final chunk down to the child
+                ing[c] += esz * data / 2
+    worst = max(max(e, i) for e, i in zip(eg, ing)) if m > 1 else 0.0
+    if pair:
+        worst += S / 2 + S / 2              # pair RS + pair AG (partner link, both directions)
+    return worst
 
 
 # ---------------------------------------------------------------------------
@@ -226,6 +379,12 @@ def main():
     scale = 1.0 / n
     cfg = hfr.Config(algo=args.algo, scale=scale, max_ctas=args.max_ctas, threads=args.threads,
                      timeout_ms=30000)
+    probe = None
+    if multi:
+        # the per-direction NVLink peak of this lease, before anything else runs
+        if rank == 0:
+            probe = nvlink_probe(n)
+        dist.barrier()
     nvls_note = None
     if multi:
         # NVLS arena (order-relaxed variant) holds the bench buffer; FLAT runs on it zero-copy too
@@ -300,33 +459,34 @@ def main():
     if comm.status() != hfr.SUCCESS:
         raise SystemExit(f"hfr error: {hfr.status_string(comm.status())}")
 
-    value = busbw(S, t_step, n)
+    value = headline(S, t_step, n, multi)
     hbm_peak, hbm_src = peaks()
     # the step's one kernel: the TMA-staged FLAT kernel for n in {2,4,8}
-    tma = os.environ.get("HFR_FLAT_TMA", "1") != "0" and n in (2, 4, 8)
-    kname = ("hfr_flat_tma_kernel" if tma else "hfr_flat_kernel") if args.algo == "flat" else "hfr_tree_kernel"
+    kname = ("hfr_flat_tma_kernel" if n in (2, 4, 8) else "hfr_flat_kernel") if args.algo == "flat" \
+        else "hfr_tree_kernel"
+    tkey = f"{kname}:{args.algo}:{n}:{dtype}:{count}:{'nvlink' if multi else 'virtual'}"
+    trec, tprov = committed_traffic(tkey)
     if multi:
         nv_bytes = 2.0 * (n - 1) / n * S   # per GPU per direction per launch (§8d)
-        roof = {"bound": "nvlink", "achieved": nv_bytes / t_step / 1e9, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
-                "frac": nv_bytes / t_step / 1e9 / NVLINK_PEER_GBS, "traffic": None,
-                "kernel": kname,
-                "algorithmic_bytes_per_launch": nv_bytes,
-                "peak_source": "measured peer copy 770 GB/s/dir (B200_PROFILING.md); 900 nominal",
-                "frac_of_nominal": nv_bytes / t_step / 1e9 / NVLINK_NOMINAL_GBS}
+        peak, peak_src = nvlink_peak(probe)
+        achieved = nv_bytes / t_step / 1e9
+        roof = {"bound": "nvlink", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "frac_of_nominal": achieved / NVLINK_NOMINAL_GBS,
+                "nominal": NVLINK_NOMINAL_GBS,
+                "traffic": (max(trec.get("nvltx_bytes", 0), trec.get("nvlrx_bytes", 0)) or None) if trec else None,
+                "traffic_kind": "ncu nvltx/nvlrx bytes per launch, the larger direction (rank 0)",
+                "dram_traffic": trec.get("dram_bytes") if trec else None,
+                "traffic_provenance": tprov,
+                "kernel": kname, "algorithmic_bytes_per_launch": nv_bytes,
+                "peak_source": peak_src, "probe_gbs": probe}
     else:
         hbm_bytes = 2.0 * n * S            # every rank's buffer read once and written once
         roof = {"bound": "hbm", "achieved": hbm_bytes / t_step / 1e9, "peak": hbm_peak, "unit": "GB/s",
-                "frac": hbm_bytes / t_step / 1e9 / hbm_peak, "traffic": None,
-                "kernel": kname,
-                "algorithmic_bytes_per_launch": hbm_bytes, "peak_source": hbm_src}
-    prof = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(prof):
-        try:
-            tr = json.load(open(prof)).get(f"{roof['kernel']}:{args.algo}:{n}:{dtype}:{'virtual' if not multi else 'nvlink'}")
-            if tr:
-                roof["traffic"] = tr
-        except (OSError, ValueError):
-            pass
+                "frac": hbm_bytes / t_step / 1e9 / hbm_peak,
+                "traffic": trec.get("dram_bytes") if trec else None,
+                "traffic_kind": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch",
+                "traffic_provenance": tprov,
+                "kernel": kname, "algorithmic_bytes_per_launch": hbm_bytes, "peak_source": hbm_src}
 
     # ---- e2e through the public API: H2D inputs, allreduce, D2H result ----
     # The copies dominate (PCIe), so the step is pipelined the way a user of
@@ -370,7 +530,7 @@ def main():
         e2e_step()
         torch.cuda.synchronize()
         t_e2e, e2e_launches = timed(e2e_step, max(1, min(args.steps, 10)))
-        e2e = {"value": busbw(S, t_e2e, n), "unit": "GB/s", "ms_per_step": t_e2e * 1e3,
+        e2e = {"value": headline(S, t_e2e, n, multi), "unit": "GB/s", "ms_per_step": t_e2e * 1e3,
                "h2d_bytes_per_step": S * len(bufs), "d2h_bytes_per_step": S,
                "note": "per step: pinned H2D of each local rank's input, hfr_allreduce, D2H of the result "
                        "(one copy per process: the ranks' results are bitwise identical), "
@@ -419,7 +579,11 @@ def main():
                 if comm.status() != hfr.SUCCESS:
                     break
                 continue
-            variants[algo] = {"busbw": busbw(S, tv, n), "ms_per_step": tv * 1e3}
+            vb = variant_dir_bytes(hfr, algo, n, S, esz)
+            variants[algo] = {"busbw": busbw(S, tv, n), "ms_per_step": tv * 1e3,
+                              "nvlink_bytes_per_dir": vb, "achieved_dir_gbs": vb / tv / 1e9,
+                              "frac_of_peak": vb / tv / 1e9 / roof["peak"],
+                              "busbw_ceiling_at_peak": busbw(S, vb / roof["peak"] / 1e9, n)}
             if algo == "nvls":
                 variants[algo]["numerics"] = "order-relaxed (NVSwitch reduction), held to DESIGN.md R18, not bit-exact"
             else:
@@ -428,12 +592,10 @@ def main():
             comm.set_config(cfg)
 
     cpu = None
-    if rank == 0 and not multi and not args.no_cpu:
-        times, cores = cpu_oracle_run(n, count, dtype, budget_s=10.0)
-        tc = statistics.median(times)
-        cpu = {"value": busbw(S, tc, n), "unit": "GB/s", "cores": cores, "kind": "oracle",
-               "sample": f"full C2 workload ({n} x {count} {dtype}), oracle/fold.c rank-ascending fold, "
-                         f"median of {len(times)} reps (~10 s), busBW-equivalent S/t*2(n-1)/n"}
+    if rank == 0 and not args.no_cpu:  # every N: rank 0, after the GPU timing (the others wait)
+        cpu = cpu_baseline(n, count, dtype, esz, multi)
+    if multi:
+        dist.barrier()
 
     if rank == 0:
         line = {
@@ -441,7 +603,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
             "config": dict(workload_config(args, n, count, dtype), clock_soak_s=args.soak),
-            "algbw": algbw(S, t_step), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "value_definition": value_definition(multi),
+            "algbw": algbw(S, t_step), "busbw_virtual": None if multi else busbw(S, t_step, n),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": ck, "nccl": nccl, "variants": variants,
         }
         print(json.dumps(line), flush=True)

@@ -34,11 +34,17 @@ def lib():
                                          ctypes.c_size_t, ctypes.c_float, ctypes.c_void_p]
         _lib.oracle_fold_bf16.argtypes = _lib.oracle_fold_f32.argtypes
         _lib.oracle_threads.restype = ctypes.c_int
+        _lib.oracle_set_threads.argtypes = [ctypes.c_int]
     return _lib
 
 
 def threads() -> int:
     return lib().oracle_threads()
+
+
+def set_threads(t: int) -> None:
+    """OpenMP threads of the folds (results are independent of it)."""
+    lib().oracle_set_threads(int(t))
 
 
 def fold_ascending(xs, scale: float = 1.0) -> np.ndarray:

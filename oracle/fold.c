@@ -43,6 +43,16 @@ int oracle_threads(void) {
 #endif
 }
 
+/* Threads the folds below use (bench.py's 1-thread cpu_baseline figure);
+ * does not change any result (OpenMP splits elements only). */
+void oracle_set_threads(int t) {
+#ifdef _OPENMP
+    if (t > 0) omp_set_num_threads(t);
+#else
+    (void)t;
+#endif
+}
+
 /* xs[r] points at rank r's count floats; out receives count floats. */
 void oracle_fold_f32(const float* const* xs, int n, size_t count, float scale, float* out) {
     long long N = (long long)count;

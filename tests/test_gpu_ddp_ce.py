@@ -157,12 +157,12 @@ def test_ddp_c5_full_size_sampled(hfr):
 @pytest.mark.parametrize("n", [2, 3, 4, 8])
 @pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16, gen.FP16])
 @pytest.mark.parametrize("N", [16_384 * 8 + 13, 1_000_003, 9_437_201])
-@pytest.mark.parametrize("mem", ["symmetric", "plain"])
+@pytest.mark.parametrize("mem", ["symmetric", "unaligned"])
 def test_ce_virtual(hfr, n, dtype, N, mem):
     """CE: copy-engine pulls (one cudaMemcpyAsync per copy), stream-memop
     ready/done/exit flags, local fold — bit-exact vs the rank-ascending fold.
-    9.4 M fp32 elements at n=2 give 2 pipeline chunks per shard; 'plain'
-    buffers are staged through the scratch first."""
+    9.4 M fp32 elements at n=2 give 2 pipeline chunks per shard; 'unaligned'
+    buffers (one element off 16 B) are staged through the scratch first."""
     comm = hfr.Comm.virtual_ranks(n, 0, hfr.Config(algo="ce", scale=0.5, timeout_ms=10000))
     try:
         launches0 = comm.launches
@@ -171,7 +171,7 @@ def test_ce_virtual(hfr, n, dtype, N, mem):
         if mem == "symmetric":
             bufs = comm.empty(N, dt)
         else:
-            bufs = [torch.empty(N, dtype=dt, device="cuda:0") for _ in range(n)]
+            bufs = [torch.empty(N + 1, dtype=dt, device="cuda:0")[1:] for _ in range(n)]
         for b, x in zip(bufs, xs):
             b.copy_(to_torch(x, "cuda:0"))
         comm.allreduce_virtual(bufs)
@@ -182,7 +182,7 @@ def test_ce_virtual(hfr, n, dtype, N, mem):
             assert_bit_exact(to_numpy(b), want, f"ce n={n} rank {r}")
         # the SMs ran one fold kernel per rank and pipeline chunk (+ the
         # staging copies for plain memory), not the single FLAT launch
-        launched = comm.launches - launches0 - (2 * n if mem == "plain" else 0)
+        launched = comm.launches - launches0 - (2 * n if mem == "unaligned" else 0)
         assert launched >= n, launched
     finally:
         comm.finalize()
