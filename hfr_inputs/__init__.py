@@ -20,6 +20,14 @@ import numpy as np
 FP32 = "f32"
 BF16 = "bf16"
 FP16 = "f16"
+E4M3 = "e4m3"
+E5M2 = "e5m2"
+FP8 = (E4M3, E5M2)
+
+# FP8 bit-pattern arrays: uint8 tagged with the format in the dtype metadata
+# (numpy has no fp8 type; the oracle reads the same tag)
+E4M3_DT = np.dtype(np.uint8, metadata={"hfr": E4M3})
+E5M2_DT = np.dtype(np.uint8, metadata={"hfr": E5M2})
 
 # Distribution names:
 #   normal     N(0, 1)
@@ -37,7 +45,8 @@ def _draw_f32(rng: np.random.Generator, dist: str, count: int, dtype: str) -> np
     if dist == "grad":
         return (rng.standard_normal(count, dtype=np.float32) * np.float32(1e-3)).astype(np.float32)
     if dist == "int":
-        lim = (1 << 20) - 1 if dtype == FP32 else 256  # bf16/fp16: exact, sums exact in fp32
+        # bf16/fp16: |x| <= 256 exact, sums exact in fp32; FP8: |x| <= 8 exact in both formats
+        lim = (1 << 20) - 1 if dtype == FP32 else (8 if dtype in FP8 else 256)
         return rng.integers(-lim, lim + 1, size=count, dtype=np.int64).astype(np.float32)
     if dist == "loguniform":
         e = rng.uniform(-20.0, 4.0, size=count)
@@ -66,6 +75,12 @@ def _to_dtype(x: np.ndarray, dtype: str) -> np.ndarray:
     if dtype == FP16:
         with np.errstate(over="ignore"):
             return np.ascontiguousarray(x, dtype=np.float32).astype(np.float16)
+    if dtype in FP8:
+        # input generation only: PyTorch's float32 -> float8 conversion of the draw
+        import torch
+        t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+        t = t.to(torch.float8_e4m3fn if dtype == E4M3 else torch.float8_e5m2)
+        return t.view(torch.uint8).numpy().view(E4M3_DT if dtype == E4M3 else E5M2_DT)
     raise ValueError(f"unknown dtype {dtype!r}")
 
 
@@ -113,4 +128,6 @@ def rank_input_torch(rank: int, count: int, dtype: str = FP32, seed_base: int = 
         return (x.view(torch.int32) >> 16).to(torch.int16).view(torch.bfloat16)  # truncation, as rank_input
     if dtype == FP16:
         return x.to(torch.float16)
+    if dtype in FP8:
+        return x.to(torch.float8_e4m3fn if dtype == E4M3 else torch.float8_e5m2)
     return x

@@ -33,10 +33,20 @@ typedef struct hfr_comm_s* hfr_comm_t;
 typedef struct hfr_req_s* hfr_req_t;
 typedef void* hfr_stream_t; /* cudaStream_t */
 
-/* Element types.  bf16 and fp16 are reduced with fp32 accumulation and ONE
- * final RNE rounding (reading R2; PAPER.md:404 lists
- * FP32/FP16/BF16/FP8). */
-typedef enum { HFR_FLOAT32 = 0, HFR_BFLOAT16 = 1, HFR_FLOAT16 = 2 } hfr_dtype_t;
+/* Element types.  bf16, fp16 and FP8 are reduced with fp32 accumulation and
+ * ONE final RNE rounding (reading R2; PAPER.md:404 lists
+ * FP32/FP16/BF16/FP8).  FP8 (reading R20): OCP E4M3 "FN" (no Inf, max 448)
+ * and E5M2 (IEEE-like, max 57344), one byte per element; a result that rounds
+ * past the largest finite value is NaN (E4M3) or +-Inf (E5M2), as
+ * torch.Tensor.to(float8_*).  FP8 runs every schedule except NVLS
+ * (UNSUPPORTED: the switch has no fp32-accumulating FP8 reduction). */
+typedef enum {
+    HFR_FLOAT32 = 0,
+    HFR_BFLOAT16 = 1,
+    HFR_FLOAT16 = 2,
+    HFR_FP8_E4M3 = 3,
+    HFR_FP8_E5M2 = 4
+} hfr_dtype_t;
 
 /* Reduction operator.  The paper's only operator is the sum ("reduction add
  * operation"). */

@@ -50,6 +50,8 @@ def set_threads(t: int) -> None:
 def fold_ascending(xs, scale: float = 1.0) -> np.ndarray:
     """C twin of hfr_oracle.fold_ascending (same contract, same bits)."""
     xs = [np.ascontiguousarray(x) for x in xs]
+    if xs[0].dtype not in (np.float32, np.uint16) or (xs[0].dtype.metadata or {}).get("hfr"):
+        raise TypeError("fold.c folds fp32 and bf16 only (use hfr_oracle for fp16 / FP8)")
     n = len(xs)
     count = xs[0].shape[0]
     ptrs = (ctypes.c_void_p * n)(*[x.ctypes.data for x in xs])

@@ -23,7 +23,10 @@ binary32 round-to-nearest-even with no FTZ/DAZ and no FMA; bf16 inputs are
 widened exactly to fp32, accumulated in fp32 and rounded ONCE to bf16 (RNE,
 NaN kept NaN) after the scale.
 
-fp32 arrays are ``np.float32``; bf16 arrays are ``np.uint16`` bit patterns.
+fp32 arrays are ``np.float32``; bf16 arrays are ``np.uint16`` bit patterns;
+fp16 arrays are ``np.float16``; FP8 arrays (PAPER.md:404 lists FP8; OCP E4M3
+"FN" and E5M2, reading R20) are ``np.uint8`` bit patterns whose dtype carries
+the format in its metadata (``E4M3_DT`` / ``E5M2_DT``).
 """
 from __future__ import annotations
 
@@ -32,6 +35,12 @@ import numpy as np
 F32 = "f32"
 BF16 = "bf16"
 F16 = "f16"
+E4M3 = "e4m3"
+E5M2 = "e5m2"
+
+# FP8 bit-pattern arrays: uint8 tagged with the format (numpy has no fp8 type)
+E4M3_DT = np.dtype(np.uint8, metadata={"hfr": E4M3})
+E5M2_DT = np.dtype(np.uint8, metadata={"hfr": E5M2})
 
 PAIR_SPLIT_ALIGN = 256  # elements; reading R13 (half boundary alignment)
 
@@ -40,9 +49,81 @@ PAIR_SPLIT_ALIGN = 256  # elements; reading R13 (half boundary alignment)
 # dtype helpers
 # ----------------------------------------------------------------------------
 
+def fp8_format(dt) -> str | None:
+    """'e4m3' / 'e5m2' for a tagged FP8 dtype, else None."""
+    md = getattr(dt, "metadata", None)
+    return md.get("hfr") if md else None
+
+
+# FP8 formats (reading R20): (exponent bits, mantissa bits, bias).  E4M3 is
+# OCP "E4M3FN": no infinities, S.1111.111 is NaN, largest finite 448; E5M2 is
+# IEEE-like: exponent 11111 holds +-Inf (mantissa 0) and NaN, largest 57344.
+_FP8 = {E4M3: (4, 3, 7), E5M2: (5, 2, 15)}
+
+
+def fp8_decode_table(fmt: str) -> np.ndarray:
+    """float64 value of each of the 256 codes, straight from the format
+    definition: normal (-1)^s 2^(e-bias) (1 + m/2^M); subnormal (e = 0)
+    (-1)^s 2^(1-bias) (m/2^M); E4M3 code S.1111.111 = NaN; E5M2 e = 2^E-1:
+    m = 0 Inf, else NaN."""
+    E, M, bias = _FP8[fmt]
+    out = np.empty(256, dtype=np.float64)
+    for code in range(256):
+        s = -1.0 if code >> 7 else 1.0
+        e = (code >> M) & ((1 << E) - 1)
+        m = code & ((1 << M) - 1)
+        if fmt == E4M3 and e == 15 and m == 7:
+            v = np.nan
+        elif fmt == E5M2 and e == 31:
+            v = np.inf if m == 0 else np.nan
+        elif e == 0:
+            v = 2.0 ** (1 - bias) * (m / 2.0 ** M)
+        else:
+            v = 2.0 ** (e - bias) * (1.0 + m / 2.0 ** M)
+        out[code] = s * v
+    return out
+
+
+def fp8_rne(y: np.ndarray, fmt: str) -> np.ndarray:
+    """fp32 -> FP8 bits, round to nearest, ties to the even code (code LSB 0).
+
+    Reading R20 (overflow, as torch.Tensor.to(float8_*): no saturation): the
+    ladder of non-negative finite values is extended by one hypothetical step
+    above the largest finite (448 + 32 = 480 for E4M3, 57344 + 8192 = 65536
+    for E5M2, whose code there is +Inf); a magnitude that rounds onto that step
+    overflows: E4M3 -> NaN (it has no Inf), E5M2 -> Inf.  NaN -> NaN;
+    +-Inf -> E5M2 +-Inf, E4M3 NaN; the sign is kept (also on zero)."""
+    E, M, bias = _FP8[fmt]
+    table = fp8_decode_table(fmt)
+    pos = [c for c in range(128) if np.isfinite(table[c])]   # 0x00.. ascending magnitudes
+    ladder = np.array([table[c] for c in pos] + [table[pos[-1]] + 2.0 ** (((pos[-1] >> M) & ((1 << E) - 1)) - bias - M)])
+    codes = np.array(pos + [pos[-1] + 1], dtype=np.int64)    # hypothetical step: next code
+    nan_code = 0x7F if fmt == E4M3 else 0x7E
+    inf_code = 0x7C
+    y = np.ascontiguousarray(y, dtype=np.float32)
+    a = np.abs(y.astype(np.float64))
+    sign = (np.signbit(y)).astype(np.int64) << 7
+    k = np.searchsorted(ladder, a, side="left")              # ladder[k-1] < a <= ladder[k]
+    k = np.clip(k, 1, len(ladder) - 1)
+    lo, hi = ladder[k - 1], ladder[k]
+    pick_hi = (a - lo > hi - a) | ((a - lo == hi - a) & ((codes[k] & 1) == 0))
+    idx = np.where(pick_hi, k, k - 1)
+    idx = np.where(a == 0, 0, idx)
+    code = codes[idx]
+    over = (idx == len(ladder) - 1) | (a > ladder[-1])
+    code = np.where(over, nan_code if fmt == E4M3 else inf_code, code)
+    code = np.where(np.isinf(y), nan_code if fmt == E4M3 else inf_code, code)
+    code = np.where(np.isnan(y), nan_code, code)
+    return (code | sign).astype(np.uint8).view(E4M3_DT if fmt == E4M3 else E5M2_DT)
+
+
 def widen(x: np.ndarray) -> np.ndarray:
     """Exact widening to fp32: bf16 bit patterns -> float32 (upper 16 bits);
-    IEEE binary16 -> float32 (every half is a float)."""
+    IEEE binary16 -> float32 (every half is a float); FP8 codes -> their
+    value from the format definition (every FP8 value is a float)."""
+    fmt = fp8_format(x.dtype)
+    if fmt:
+        return fp8_decode_table(fmt).astype(np.float32)[np.asarray(x).view(np.uint8)]
     if x.dtype == np.float32:
         return x
     if x.dtype == np.uint16:
@@ -80,10 +161,15 @@ def _finish(acc: np.ndarray, scale: float, out_dtype: str) -> np.ndarray:
         return bf16_rne(y)
     if out_dtype == F16:
         return y.astype(np.float16)  # numpy's float32 -> binary16 conversion rounds to nearest even
+    if out_dtype in (E4M3, E5M2):
+        return fp8_rne(y, out_dtype)
     raise ValueError(out_dtype)
 
 
 def _out_dtype(xs) -> str:
+    fmt = fp8_format(xs[0].dtype)
+    if fmt:
+        return fmt
     if xs[0].dtype == np.uint16:
         return BF16
     if xs[0].dtype == np.float16:
@@ -92,7 +178,7 @@ def _out_dtype(xs) -> str:
 
 
 def _out_np(out_dtype: str):
-    return {F32: np.float32, BF16: np.uint16, F16: np.float16}[out_dtype]
+    return {F32: np.float32, BF16: np.uint16, F16: np.float16, E4M3: E4M3_DT, E5M2: E5M2_DT}[out_dtype]
 
 
 # ----------------------------------------------------------------------------
@@ -267,7 +353,8 @@ def shard_bounds(count: int, n: int, elems_per_vec: int):
 
 
 def _k(xs):
-    return 4 if xs[0].dtype == np.float32 else 8
+    """Elements per 16-byte vector."""
+    return 16 // xs[0].dtype.itemsize
 
 
 def reduce_scatter(xs, scale: float = 1.0):

@@ -26,7 +26,7 @@ SUCCESS, ERR_INVALID_ARGUMENT, ERR_UNSUPPORTED, ERR_CUDA, ERR_OUT_OF_MEMORY, ERR
 ALGO_AUTO, ALGO_FLAT, ALGO_DBT, ALGO_PAIR_DBT, ALGO_ONESHOT, ALGO_CE, ALGO_NVLS = range(7)
 ALGOS = {"auto": ALGO_AUTO, "flat": ALGO_FLAT, "dbt": ALGO_DBT, "pair_dbt": ALGO_PAIR_DBT, "oneshot": ALGO_ONESHOT,
          "ce": ALGO_CE, "nvls": ALGO_NVLS}
-FLOAT32, BFLOAT16, FLOAT16 = 0, 1, 2
+FLOAT32, BFLOAT16, FLOAT16, FP8_E4M3, FP8_E5M2 = 0, 1, 2, 3, 4
 SUM = 0
 ALLREDUCE, REDUCE_SCATTER, ALLGATHER, REDUCE, BROADCAST = range(5)
 COLLS = {"allreduce": ALLREDUCE, "reduce_scatter": REDUCE_SCATTER, "allgather": ALLGATHER, "reduce": REDUCE,
@@ -159,7 +159,8 @@ def tree_query(n: int, which: int):
 def shard_range(nranks: int, count: int, dtype: str, rank: int):
     """[lo, hi) of rank's shard (hfr_shard_range; dtype 'f32' or 'bf16')."""
     lo, hi = ctypes.c_size_t(), ctypes.c_size_t()
-    code = {"bf16": BFLOAT16, "bfloat16": BFLOAT16, "f16": FLOAT16, "float16": FLOAT16}.get(dtype, FLOAT32)
+    code = {"bf16": BFLOAT16, "bfloat16": BFLOAT16, "f16": FLOAT16, "float16": FLOAT16, "e4m3": FP8_E4M3,
+            "e5m2": FP8_E5M2}.get(dtype, FLOAT32)
     _check(_lib().hfr_shard_range(nranks, count, code, rank, ctypes.byref(lo), ctypes.byref(hi)), "hfr_shard_range")
     return lo.value, hi.value
 
@@ -172,7 +173,11 @@ def _dtype_code(t) -> int:
         return BFLOAT16
     if t.dtype == torch.float16:
         return FLOAT16
-    raise TypeError(f"hfr supports float32, bfloat16 and float16, not {t.dtype}")
+    if t.dtype == torch.float8_e4m3fn:
+        return FP8_E4M3
+    if t.dtype == torch.float8_e5m2:
+        return FP8_E5M2
+    raise TypeError(f"hfr supports float32, bfloat16, float16, float8_e4m3fn and float8_e5m2, not {t.dtype}")
 
 
 def _stream_handle(stream) -> int:

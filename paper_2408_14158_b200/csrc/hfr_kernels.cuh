@@ -390,6 +390,92 @@ struct F16 {
   __device__ static __forceinline__ float from_bits(uint32_t b) { return h2f(b); }
 };
 
+// FP8 (PAPER.md:404 lists FP8; reading R20): OCP E4M3 ("FN": no Inf, NaN =
+// S.1111.111, max 448) and E5M2 (IEEE-like, max 57344).  Widened exactly
+// (every FP8 value is a binary16, hence a float: cvt.rn.f16x2.e4m3x2 /
+// .e5m2x2), fp32 accumulate, one RNE rounding.  The hardware converts with
+// .satfinite only, so the overflow rule of R20 (as torch.Tensor.to: no
+// saturation) is applied on top: a magnitude that rounds past the largest
+// finite value becomes NaN (E4M3, which has no Inf: |x| > 464, the tie 464
+// rounding down to 448) or +-Inf (E5M2: |x| >= 61440, the tie rounding up
+// to the next power of two); NaN stays NaN.
+template <bool kE5M2>
+struct FP8 {
+  using T = uint8_t;
+  static constexpr int kPerVec = 16;
+  __device__ static __forceinline__ uint32_t cvt2_to_h2(uint32_t two) {  // 2 codes (low 16 bits) -> f16x2
+    uint32_t h2;
+    const uint16_t x = (uint16_t)two;
+    if constexpr (kE5M2)
+      asm("cvt.rn.f16x2.e5m2x2 %0, %1;" : "=r"(h2) : "h"(x));
+    else
+      asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(x));
+    return h2;
+  }
+  __device__ static __forceinline__ void widen2(uint32_t two, float* f) {
+    const uint32_t h2 = cvt2_to_h2(two);
+    f[0] = __half2float(__ushort_as_half((unsigned short)(h2 & 0xFFFFu)));
+    f[1] = __half2float(__ushort_as_half((unsigned short)(h2 >> 16)));
+  }
+  __device__ static __forceinline__ void widen(const uint4& v, float* f) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      widen2(w[j] & 0xFFFFu, f + 4 * j);
+      widen2(w[j] >> 16, f + 4 * j + 2);
+    }
+  }
+  // 8 codes (8 bytes) -> 8 floats / back (the tree kernel's 8-element unit)
+  __device__ static __forceinline__ void widen8(const uint2& v, float* f) {
+    widen2(v.x & 0xFFFFu, f);
+    widen2(v.x >> 16, f + 2);
+    widen2(v.y & 0xFFFFu, f + 4);
+    widen2(v.y >> 16, f + 6);
+  }
+  __device__ static __forceinline__ uint32_t fix(uint32_t code, float x) {  // R20 overflow rule
+    const float a = fabsf(x);
+    const uint32_t sign = (__float_as_uint(x) >> 24) & 0x80u;
+    if constexpr (kE5M2) {
+      if (a != a) return 0x7Eu | sign;
+      if (a >= 61440.f) return 0x7Cu | sign;
+    } else {
+      if (!(a <= 464.f)) return 0x7Fu | sign;  // NaN, Inf or overflow
+    }
+    return code;
+  }
+  __device__ static __forceinline__ uint32_t rne2(float lo, float hi) {  // -> 2 codes in the low 16 bits
+    uint16_t st;
+    if constexpr (kE5M2)
+      asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(st) : "f"(hi), "f"(lo));
+    else
+      asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(st) : "f"(hi), "f"(lo));
+    return fix(st & 0xFFu, lo) | (fix((uint32_t)st >> 8, hi) << 8);
+  }
+  __device__ static __forceinline__ uint32_t rne(float x) { return rne2(x, 0.f) & 0xFFu; }
+  __device__ static __forceinline__ uint4 narrow(const float* f) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[j] = rne2(f[4 * j], f[4 * j + 1]) | (rne2(f[4 * j + 2], f[4 * j + 3]) << 16);
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  __device__ static __forceinline__ uint2 narrow8(const float* f) {
+    return make_uint2(rne2(f[0], f[1]) | (rne2(f[2], f[3]) << 16), rne2(f[4], f[5]) | (rne2(f[6], f[7]) << 16));
+  }
+  __device__ static __forceinline__ float from_bits(uint32_t b) {
+    float f[2];
+    widen2(b & 0xFFu, f);
+    return f[0];
+  }
+  __device__ static __forceinline__ float load1(const char* p, uint64_t i) {
+    return from_bits(reinterpret_cast<const uint8_t*>(p)[i]);
+  }
+  __device__ static __forceinline__ void store1(char* p, uint64_t i, float v) {
+    reinterpret_cast<uint8_t*>(p)[i] = (uint8_t)rne(v);
+  }
+};
+using E4M3 = FP8<false>;
+using E5M2 = FP8<true>;
+
 // ---------------------------------------------------------------------------
 // Subsystems (1)+(3), FLAT: fused reduce-scatter + all-gather/cast/scale.
 //
@@ -527,8 +613,12 @@ __global__ void __launch_bounds__(512) hfr_flat_kernel(const Args a) {
     if (own == nown - 1 && b == 0 && threadIdx.x < a.count - t0) {
       const uint64_t el = t0 + threadIdx.x;
       if (src >= 0) {
-        // raw copy of the element (bf16 bits or fp32 bits)
-        if constexpr (K == 8) {
+        // raw copy of the element (fp8 / 16-bit / fp32 bits)
+        if constexpr (K == 16) {
+          const uint8_t x = reinterpret_cast<const uint8_t*>(a.buf[src])[el];
+          for (int r = 0; r < n; ++r)
+            if ((dmask >> r) & 1u) reinterpret_cast<uint8_t*>(a.buf[r])[el] = x;
+        } else if constexpr (K == 8) {
           const uint16_t x = reinterpret_cast<const uint16_t*>(a.buf[src])[el];
           for (int r = 0; r < n; ++r)
             if ((dmask >> r) & 1u) reinterpret_cast<uint16_t*>(a.buf[r])[el] = x;
@@ -786,6 +876,7 @@ __device__ __forceinline__ uint4 ld128_volatile(const void* p) {
 
 template <class E>
 __device__ __forceinline__ uint32_t elem_bits(const char* p, uint64_t e) {
+  if constexpr (E::kPerVec == 16) return reinterpret_cast<const uint8_t*>(p)[e];
   if constexpr (E::kPerVec == 8) return reinterpret_cast<const uint16_t*>(p)[e];
   return reinterpret_cast<const uint32_t*>(p)[e];
 }
@@ -1116,16 +1207,32 @@ __global__ void __launch_bounds__(512) hfr_nvls_kernel(const Args a) {
 template <class E>
 __device__ __forceinline__ void load8(const char* base, uint64_t e, float* f) {
   // 8 consecutive elements starting at element e (e % 8 == 0)
-  if constexpr (E::kPerVec == 8) {
+  if constexpr (E::kPerVec == 16) {
+    E::widen8(*reinterpret_cast<const uint2*>(base + e), f);
+  } else if constexpr (E::kPerVec == 8) {
     E::widen(ld128(base + e * 2), f);
   } else {
     E::widen(ld128(base + e * 4), f);
     E::widen(ld128(base + e * 4 + 16), f + 4);
   }
 }
+// the same from any address space (the PAIR kernel's shared-memory ring)
+template <class E>
+__device__ __forceinline__ void widen8_generic(const uint8_t* p, float* f) {
+  if constexpr (E::kPerVec == 16) {
+    E::widen8(*reinterpret_cast<const uint2*>(p), f);
+  } else if constexpr (E::kPerVec == 8) {
+    E::widen(*reinterpret_cast<const uint4*>(p), f);
+  } else {
+    E::widen(*reinterpret_cast<const uint4*>(p), f);
+    E::widen(*reinterpret_cast<const uint4*>(p + 16), f + 4);
+  }
+}
 template <class E>
 __device__ __forceinline__ void store8(char* base, uint64_t e, const float* f) {
-  if constexpr (E::kPerVec == 8) {
+  if constexpr (E::kPerVec == 16) {
+    *reinterpret_cast<uint2*>(base + e) = E::narrow8(f);
+  } else if constexpr (E::kPerVec == 8) {
     st128(base + e * 2, E::narrow(f));
   } else {
     st128(base + e * 4, E::narrow(f));
@@ -1205,7 +1312,11 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
       }
     }
     for (uint64_t y = b0 + nv * 16 + threadIdx.x * esz; y < b1; y += (uint64_t)blockDim.x * esz) {
-      if (esz == 2) {
+      if (esz == 1) {
+        const uint8_t val = *reinterpret_cast<const uint8_t*>(mybuf + y);
+        for (int k = 0; k < nd.nchild; ++k) *reinterpret_cast<uint8_t*>(a.buf[member(nd.child[k])] + y) = val;
+        if constexpr (PAIR) *reinterpret_cast<uint8_t*>(a.buf[partner] + y) = val;
+      } else if (esz == 2) {
         const uint16_t val = *reinterpret_cast<const uint16_t*>(mybuf + y);
         for (int k = 0; k < nd.nchild; ++k) *reinterpret_cast<uint16_t*>(a.buf[member(nd.child[k])] + y) = val;
         if constexpr (PAIR) *reinterpret_cast<uint16_t*>(a.buf[partner] + y) = val;
@@ -1251,10 +1362,13 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
       constexpr uint64_t esz = sizeof(typename E::T);
       const uint64_t nvc = (pe1 - pe0) / 8;
       const uint64_t u0 = j * kPairSubUnits, u1 = u0 + kPairSubUnits < nvc ? u0 + kPairSubUnits : nvc;
-      const uint32_t bytes = (uint32_t)((u1 - u0) * 8 * esz);
+      // bulk copies move whole 16-byte units: an odd last FP8 unit (8 bytes)
+      // is read directly from the partner below
+      const uint32_t bytes = (uint32_t)((u1 - u0) * 8 * esz) & ~15u;
       mbar_expect_tx(&pbar[st], bytes);
-      bulk_g2s(pstage + (size_t)st * kPairSubUnits * 8 * esz, a.buf[partner] + (base + pe0 + u0 * 8) * esz, bytes,
-               &pbar[st]);
+      if (bytes)
+        bulk_g2s(pstage + (size_t)st * kPairSubUnits * 8 * esz, a.buf[partner] + (base + pe0 + u0 * 8) * esz, bytes,
+                 &pbar[st]);
     };
     if constexpr (PAIR) {
       if (threadIdx.x == 0)
@@ -1274,7 +1388,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     // A DBT leaf's partial is its own x: stream it as a copy with 4 x 16 B in
     // flight per thread (r01: DBT n=4 313 -> 360-378 GB/s).  bf16 leaves send
     // their raw bf16 (the parent widens exactly), halving leaf traffic.
-    const bool leafcopy = !PAIR && nchild == 0 && !root;
+    const bool leafcopy = !PAIR && nchild == 0 && !root && E::kPerVec <= 8;  // FP8 leaves go through unit()
     // slot sl of this node holds a raw-bf16 leaf partial?
     bool slot_bf16[2] = {false, false};
     if constexpr (!PAIR && E::kPerVec == 8) {
@@ -1367,8 +1481,10 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
         const uint8_t* sm = pstage + (size_t)st * kPairSubUnits * 8 * esz;
         for (uint64_t v = u0 + threadIdx.x; v < u1; v += blockDim.x) {
           float xp[8];
-          E::widen(*reinterpret_cast<const uint4*>(sm + (v - u0) * 8 * esz), xp);
-          if constexpr (esz == 4) E::widen(*reinterpret_cast<const uint4*>(sm + (v - u0) * 32 + 16), xp + 4);
+          if ((v - u0 + 1) * 8 * esz <= (((u1 - u0) * 8 * esz) & ~(uint64_t)15))
+            widen8_generic<E>(sm + (v - u0) * 8 * esz, xp);  // shared memory: generic loads
+          else
+            widen8_generic<E>(reinterpret_cast<const uint8_t*>(pbuf) + (base + e0 + v * 8) * esz, xp);
           unit(v, xp);
         }
         __syncthreads();  // stage st consumed

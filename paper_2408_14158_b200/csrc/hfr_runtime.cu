@@ -219,11 +219,18 @@ uint64_t fnv(uint64_t h, uint64_t v) {
   return h;
 }
 
-size_t dtype_size(hfr_dtype_t t) { return t == HFR_FLOAT32 ? 4 : 2; }
+size_t dtype_size(hfr_dtype_t t) { return t == HFR_FLOAT32 ? 4 : (t == HFR_FP8_E4M3 || t == HFR_FP8_E5M2) ? 1 : 2; }
+bool dtype_valid(int t) { return t >= HFR_FLOAT32 && t <= HFR_FP8_E5M2; }
+bool dtype_fp8(hfr_dtype_t t) { return t == HFR_FP8_E4M3 || t == HFR_FP8_E5M2; }
+uint64_t per_vec(hfr_dtype_t t) { return 16 / dtype_size(t); }  // elements per 16 bytes
 
 // Kernel instantiation by element type: HFR_BY_DTYPE(dt, M) expands M(F32),
 // M(BF16) or M(F16).
-#define HFR_BY_DTYPE(dt, M) ((dt) == HFR_BFLOAT16 ? (M(BF16)) : (dt) == HFR_FLOAT16 ? (M(F16)) : (M(F32)))
+#define HFR_BY_DTYPE(dt, M)                                                                          \
+  ((dt) == HFR_BFLOAT16 ? (M(BF16)) : (dt) == HFR_FLOAT16 ? (M(F16)) : (dt) == HFR_FP8_E4M3 ? (M(E4M3)) \
+   : (dt) == HFR_FP8_E5M2 ? (M(E5M2)) : (M(F32)))
+// NVLS has no fp32-accumulating multimem form for FP8 (UNSUPPORTED there)
+#define HFR_BY_DTYPE_NO_FP8(dt, M) ((dt) == HFR_BFLOAT16 ? (M(BF16)) : (dt) == HFR_FLOAT16 ? (M(F16)) : (M(F32)))
 
 // An explicit ONESHOT on a message above oneshot_max_bytes runs FLAT (same
 // result bits).
@@ -641,7 +648,7 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
   }
   int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : per_sm * c->num_sms;
   // no more CTAs than tiles: idle CTAs would only add handshakes
-  const uint64_t per = dt == HFR_FLOAT32 ? 4 : 8;
+  const uint64_t per = per_vec(dt);
   const uint64_t tiles = (count / per / c->n + (uint64_t)tile / 16 - 1) / ((uint64_t)tile / 16) + 1;
   g = (int)std::min<uint64_t>((uint64_t)g, tiles);
   if (c->virt && c->local > 1) {
@@ -680,7 +687,7 @@ hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
 #define HFR_FLAT_FN(E) flat_fn<E>(c->n)
   const void* fn = HFR_BY_DTYPE(dt, HFR_FLAT_FN);
   const int threads = cta_threads(c, 512);
-  const uint64_t per = dt == HFR_FLOAT32 ? 4 : 8;
+  const uint64_t per = per_vec(dt);
   const uint64_t vec_per_rank = count / per / c->n + 1;
   int g = 0;
   HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>((vec_per_rank + threads - 1) / threads, kMaxCtas), &g));
@@ -776,7 +783,7 @@ hfr_status_t run_oneshot(hfr_comm_s* c, char* const* local_bufs, uint64_t count,
     return run_oneshot_ll(c, local_bufs, count, dt, sig, s);
 #define HFR_ONESHOT_FN(E) (const void*)hfr_oneshot_kernel<E, 0>
   const void* fn = HFR_BY_DTYPE(dt, HFR_ONESHOT_FN);
-  const uint64_t per = dt == HFR_FLOAT32 ? 4 : 8;
+  const uint64_t per = per_vec(dt);
   const uint64_t nvec = count / per;
   // small grids: one CTA per 2048 vectors (32 KiB), at least n threads
   const int min_thr = 32 * ((c->n + 31) / 32);
@@ -983,6 +990,10 @@ hfr_status_t run_ce(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_
           hfr_local_fold_kernel<BF16><<<ctas, 512, 0, fs[l]>>>(f);
         else if (dt == HFR_FLOAT16)
           hfr_local_fold_kernel<F16><<<ctas, 512, 0, fs[l]>>>(f);
+        else if (dt == HFR_FP8_E4M3)
+          hfr_local_fold_kernel<E4M3><<<ctas, 512, 0, fs[l]>>>(f);
+        else if (dt == HFR_FP8_E5M2)
+          hfr_local_fold_kernel<E5M2><<<ctas, 512, 0, fs[l]>>>(f);
         else
           hfr_local_fold_kernel<F32><<<ctas, 512, 0, fs[l]>>>(f);
         cudaError_t err = cudaGetLastError();
@@ -1037,9 +1048,10 @@ hfr_status_t run_nvls(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
                       cudaStream_t s, int coll = HFR_ALLREDUCE, int root = 0) {
 #define HFR_NVLS_FN(E) (const void*)hfr_nvls_kernel<E>
 #define HFR_NVLS_COLL_FN(E) (const void*)hfr_nvls_coll_kernel<E>
-  const void* fn = coll == HFR_ALLREDUCE ? HFR_BY_DTYPE(dt, HFR_NVLS_FN) : HFR_BY_DTYPE(dt, HFR_NVLS_COLL_FN);
+  if (dtype_fp8(dt)) return HFR_ERR_UNSUPPORTED;
+  const void* fn = coll == HFR_ALLREDUCE ? HFR_BY_DTYPE_NO_FP8(dt, HFR_NVLS_FN) : HFR_BY_DTYPE_NO_FP8(dt, HFR_NVLS_COLL_FN);
   const int threads = cta_threads(c, 512);
-  const uint64_t per = dt == HFR_FLOAT32 ? 4 : 8;
+  const uint64_t per = per_vec(dt);
   // reduce / broadcast: the root alone moves the whole buffer
   const bool solo = coll == HFR_REDUCE || coll == HFR_BROADCAST;
   const uint64_t vec_per_rank = count / per / (solo ? 1 : c->n) + 1;
@@ -1104,7 +1116,7 @@ hfr_status_t allreduce_impl(hfr_comm_s* c, char* const* local_bufs, size_t count
                             cudaStream_t user, hfr_req_t* req, int coll = HFR_ALLREDUCE, int root = 0) {
   if (!c) return HFR_ERR_NOT_INITIALIZED;
   if (req) *req = nullptr;
-  if (dt != HFR_FLOAT32 && dt != HFR_BFLOAT16 && dt != HFR_FLOAT16) return HFR_ERR_INVALID_ARGUMENT;
+  if (!dtype_valid(dt)) return HFR_ERR_INVALID_ARGUMENT;
   if (coll < HFR_ALLREDUCE || coll > HFR_BROADCAST) return HFR_ERR_INVALID_ARGUMENT;
   if ((coll == HFR_REDUCE || coll == HFR_BROADCAST) && (root < 0 || root >= c->n)) return HFR_ERR_INVALID_ARGUMENT;
   if (op != HFR_SUM) return HFR_ERR_UNSUPPORTED;
@@ -1411,9 +1423,9 @@ hfr_status_t hfr_collective_virtual(hfr_comm_t c, hfr_coll_t coll, void* const* 
 
 hfr_status_t hfr_shard_range(int nranks, size_t count, hfr_dtype_t dtype, int rank, size_t* lo, size_t* hi) {
   if (nranks < 1 || nranks > HFR_MAX_RANKS || rank < 0 || rank >= nranks || !lo || !hi ||
-      (dtype != HFR_FLOAT32 && dtype != HFR_BFLOAT16 && dtype != HFR_FLOAT16))
+      !dtype_valid(dtype))
     return HFR_ERR_INVALID_ARGUMENT;
-  const uint64_t K = dtype == HFR_FLOAT32 ? 4 : 8;  // elements per 16-byte vector
+  const uint64_t K = per_vec(dtype);  // elements per 16-byte vector
   const uint64_t nvec = count / K;
   *lo = K * (nvec * (uint64_t)rank / nranks);
   *hi = rank == nranks - 1 ? count : K * (nvec * (uint64_t)(rank + 1) / nranks);

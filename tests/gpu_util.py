@@ -6,26 +6,53 @@ import numpy as np
 import hfr_inputs as gen
 
 
+def _fp8(x: np.ndarray):
+    md = x.dtype.metadata
+    return md.get("hfr") if md else None
+
+
 def to_torch(x: np.ndarray, device):
     import torch
+    fmt = _fp8(x)
+    if fmt:
+        t = torch.from_numpy(np.ascontiguousarray(x).view(np.uint8))
+        return t.view(torch.float8_e4m3fn if fmt == gen.E4M3 else torch.float8_e5m2).to(device)
     if x.dtype == np.uint16:
         return torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to(device)
     return torch.from_numpy(x).to(device)
 
 
+def dtype_of(x: np.ndarray) -> str:
+    """The hfr_inputs dtype name of an input array."""
+    fmt = _fp8(x)
+    if fmt:
+        return fmt
+    return {np.dtype(np.uint16): gen.BF16, np.dtype(np.float16): gen.FP16}.get(x.dtype, gen.FP32)
+
+
 def torch_dtype(dtype: str):
     import torch
-    return {gen.BF16: torch.bfloat16, gen.FP16: torch.float16}.get(dtype, torch.float32)
+    return {gen.BF16: torch.bfloat16, gen.FP16: torch.float16, gen.E4M3: torch.float8_e4m3fn,
+            gen.E5M2: torch.float8_e5m2}.get(dtype, torch.float32)
 
 
 def to_numpy(t) -> np.ndarray:
     import torch
     if t.dtype == torch.bfloat16:
         return t.detach().cpu().view(torch.int16).numpy().view(np.uint16)
+    if t.dtype == torch.float8_e4m3fn:
+        return t.detach().cpu().view(torch.uint8).numpy().view(gen.E4M3_DT)
+    if t.dtype == torch.float8_e5m2:
+        return t.detach().cpu().view(torch.uint8).numpy().view(gen.E5M2_DT)
     return t.detach().cpu().numpy()
 
 
 def as_f32(x: np.ndarray) -> np.ndarray:
+    fmt = _fp8(x)
+    if fmt:
+        import torch
+        t = torch.from_numpy(np.ascontiguousarray(x).view(np.uint8))
+        return t.view(torch.float8_e4m3fn if fmt == gen.E4M3 else torch.float8_e5m2).float().numpy()
     if x.dtype == np.uint16:
         return (x.astype(np.uint32) << np.uint32(16)).view(np.float32)
     if x.dtype == np.float16:
@@ -34,7 +61,7 @@ def as_f32(x: np.ndarray) -> np.ndarray:
 
 
 def _bits(x: np.ndarray) -> np.ndarray:
-    return x.view(np.uint16 if x.dtype.itemsize == 2 else np.uint32)
+    return x.view({1: np.uint8, 2: np.uint16}.get(x.dtype.itemsize, np.uint32))
 
 
 def assert_bit_exact(got: np.ndarray, want: np.ndarray, what: str = ""):

@@ -11,7 +11,7 @@ import pytest
 
 import hfr_inputs as gen
 from oracle import hfr_oracle as O
-from tests.gpu_util import assert_bit_exact, to_numpy, to_torch, torch_dtype
+from tests.gpu_util import assert_bit_exact, dtype_of, to_numpy, to_torch, torch_dtype
 
 pytestmark = pytest.mark.gpu
 
@@ -40,7 +40,7 @@ def comm_for(hfr, n):
 def run(hfr, n, xs, algo, chunk=512, scale=1.0, symmetric=True, offset=0, async_op=False):
     comm = comm_for(hfr, n)
     comm.set_config(hfr.Config(algo=algo, chunk_elems=chunk, scale=scale))
-    dt = torch_dtype({np.dtype(np.uint16): gen.BF16, np.dtype(np.float16): gen.FP16}.get(xs[0].dtype, gen.FP32))
+    dt = torch_dtype(dtype_of(xs[0]))
     N = xs[0].shape[0]
     if symmetric:
         bufs = [b[offset:offset + N] for b in comm.empty(N + offset, dt)]
@@ -333,3 +333,55 @@ def test_oneshot_fenced_form(hfr, n, dtype):
     xs = gen.rank_inputs(n, N, dtype, "normal", seed_base=91)
     outs = run(hfr, n, xs, "oneshot", scale=0.5)
     check(outs, O.allreduce(xs, "flat", scale=0.5)[0], f"fenced oneshot n={n}")
+
+
+FP8S = [gen.E4M3, gen.E5M2]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("dtype", FP8S)
+@pytest.mark.parametrize("algo", ALGOS + ["ce", "auto"])
+@pytest.mark.parametrize("N", [7, 4096 + 13, 100_003, 1_000_001])
+def test_parity_fp8(hfr, n, dtype, algo, N):
+    """FP8 (reading R20): E4M3 / E5M2 inputs widened exactly,
+    fp32 accumulate in the schedule's order, one RNE rounding with the R20
+    overflow rule — bit-exact vs the oracle for every schedule."""
+    if algo == "pair_dbt" and n % 2:
+        pytest.skip("pair-first needs even n")
+    xs = gen.rank_inputs(n, N, dtype, "normal", seed_base=2100 + N)
+    outs = run(hfr, n, xs, algo, chunk=512, scale=0.5)
+    check(outs, O.allreduce(xs, algo, chunk_elems=512, scale=0.5)[0], f"{algo} n={n} {dtype} N={N}")
+
+
+@pytest.mark.parametrize("dtype", FP8S)
+@pytest.mark.parametrize("dist", ["specials", "int", "loguniform", "grad"])
+@pytest.mark.parametrize("algo", ALGOS + ["ce"])
+@pytest.mark.parametrize("scale", [1.0, 0.125, 40.0])
+def test_parity_fp8_distributions(hfr, dtype, dist, algo, scale):
+    """FP8 value mixes incl. NaN/Inf/subnormals/signed zeros, and a scale of
+    40 that drives sums past the largest finite value (E4M3 -> NaN, E5M2 ->
+    Inf under R20)."""
+    n, N = 8, 3 * 16384 + 5
+    xs = gen.rank_inputs(n, N, dtype, dist, seed_base=88)
+    outs = run(hfr, n, xs, algo, chunk=256, scale=scale)
+    check(outs, O.allreduce(xs, algo, chunk_elems=256, scale=scale)[0], f"{algo} {dist} {dtype} x{scale}")
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("dtype", FP8S)
+@pytest.mark.parametrize("kind", ["reduce_scatter", "allgather", "reduce", "broadcast"])
+def test_collectives_fp8(hfr, n, dtype, kind):
+    comm = comm_for(hfr, n)
+    comm.set_config(hfr.Config(scale=0.5))
+    N = 300_007
+    xs = gen.rank_inputs(n, N, dtype, "normal", seed_base=400)
+    bufs = comm.empty(N, torch_dtype(dtype))
+    for b, x in zip(bufs, xs):
+        b.copy_(to_torch(x, "cuda:0"))
+    comm.collective_virtual(kind, bufs, root=1)
+    torch.cuda.synchronize()
+    assert comm.status() == hfr.SUCCESS
+    want = {"reduce_scatter": lambda: O.reduce_scatter(xs, 0.5), "allgather": lambda: O.all_gather(xs),
+            "reduce": lambda: O.reduce(xs, 1, 0.5), "broadcast": lambda: O.broadcast(xs, 1)}[kind]()
+    for r, b in enumerate(bufs):
+        assert_bit_exact(to_numpy(b), want[r], f"{kind} fp8 n={n} rank {r}")

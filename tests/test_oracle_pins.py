@@ -102,7 +102,7 @@ def exact_mul(a: float, b: float) -> float:
 def exact_bf16(y: float) -> float:
     if math.isnan(y) or math.isinf(y) or y == 0:
         return y
-    return float(bf16_round(Fraction(y)))
+    return math.copysign(float(bf16_round(Fraction(y))), y)  # an underflow to zero keeps the sign
 
 
 def bits32(x) -> np.ndarray:
@@ -470,7 +470,7 @@ def f16_round(q: Fraction):
 def exact_f16(y: float) -> float:
     if math.isnan(y) or math.isinf(y) or y == 0:
         return y
-    return float(f16_round(Fraction(y)))
+    return math.copysign(float(f16_round(Fraction(y))), y)  # an underflow to zero keeps the sign
 
 
 @pytest.mark.parametrize("n", [1, 2, 4, 8])
@@ -513,3 +513,107 @@ def test_integer_closed_form_fp16(n, algo):
     want = sum(x.astype(np.int64) for x in xs)
     got = O.allreduce(xs, algo, chunk_elems=256)[0]
     assert np.array_equal(got.astype(np.int64), want)
+
+
+# ----------------------------------------------------------------------------
+# FP8 (PAPER.md:404 lists FP8; reading R20): E4M3 (OCP "FN") and E5M2, fp32
+# accumulate, one RNE rounding; overflow -> NaN (E4M3) / Inf (E5M2)
+# ----------------------------------------------------------------------------
+
+FP8_FORMATS = [(gen.E4M3, "float8_e4m3fn"), (gen.E5M2, "float8_e5m2")]
+
+
+def exact_fp8(y: float, fmt: str) -> float:
+    """RNE of a float to the FP8 format from exact rationals (independent of
+    the oracle's ladder search): E4M3 p=4, emin=-6, largest finite 448 (the
+    binary grid's 480 is the NaN code); E5M2 p=3, emin=-14, emax=15."""
+    if math.isnan(y):
+        return math.nan
+    if fmt == gen.E4M3:
+        if math.isinf(y):
+            return math.nan
+        if y == 0:
+            return y
+        r = _round_binary(Fraction(y), 4, -6, 8)
+        return math.nan if (math.isinf(r) or abs(r) > 448) else math.copysign(float(r), y)
+    if math.isinf(y) or y == 0:
+        return y
+    return math.copysign(float(_round_binary(Fraction(y), 3, -14, 15)), y)  # signed zero on underflow
+
+
+def _torch_fp8_values(codes: np.ndarray, tname: str) -> np.ndarray:
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(codes).view(np.uint8)).view(getattr(torch, tname)).float().numpy()
+
+
+@pytest.mark.parametrize("fmt,tname", FP8_FORMATS)
+def test_fp8_decode_matches_torch(fmt, tname):
+    codes = np.arange(256, dtype=np.uint8)
+    want = _torch_fp8_values(codes, tname)
+    got = O.fp8_decode_table(fmt).astype(np.float32)
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    m = ~np.isnan(want)
+    assert np.array_equal(bits32(got[m]), bits32(want[m]))
+
+
+@pytest.mark.parametrize("fmt,tname", FP8_FORMATS)
+def test_fp8_rne_matches_torch_and_hand_cases(fmt, tname):
+    import torch
+    rng = np.random.default_rng(3)
+    f = rng.integers(0, 2 ** 32, size=1 << 20, dtype=np.uint64).astype(np.uint32).view(np.float32)
+    f2 = (rng.standard_normal(1 << 20) * np.exp2(rng.uniform(-20, 18, 1 << 20))).astype(np.float32)
+    for y in (f, f2):
+        got = O.fp8_rne(y, fmt).view(np.uint8)
+        want = torch.from_numpy(y).to(getattr(torch, tname)).view(torch.uint8).numpy()
+        gv, wv = O.fp8_decode_table(fmt)[got], O.fp8_decode_table(fmt)[want]
+        assert np.array_equal(np.isnan(gv), np.isnan(wv))
+        m = ~np.isnan(wv)
+        assert np.array_equal(got[m], want[m])
+    if fmt == gen.E4M3:  # ties to even code, the 464 tie stays finite, past it NaN; subnormal ties
+        cases = [(464.0, 448.0), (465.0, math.nan), (1e9, math.nan), (math.inf, math.nan), (2.0 ** -10, 0.0),
+                 (1.5 * 2.0 ** -9, 2.0 ** -8), (17.0, 16.0), (19.0, 20.0)]
+    else:
+        cases = [(61439.0, 57344.0), (61440.0, math.inf), (-math.inf, -math.inf), (2.0 ** -17, 0.0),
+                 (1.5 * 2.0 ** -16, 2.0 ** -15), (9.0, 8.0), (11.0, 12.0)]
+    for v, w in cases:
+        g = float(O.widen(O.fp8_rne(np.array([v], np.float32), fmt))[0])
+        assert (math.isnan(g) and math.isnan(w)) or g == w, (fmt, v, g, w)
+        e = exact_fp8(v, fmt)
+        assert (math.isnan(e) and math.isnan(w)) or e == w, (fmt, v, e, w)
+
+
+@pytest.mark.parametrize("fmt,tname", FP8_FORMATS)
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("dist", ["normal", "loguniform", "specials", "int"])
+def test_fold_ascending_fp8_brute_force(fmt, tname, n, dist):
+    """Exact-rational brute force of the rank-ascending fold
+    with FP8 inputs decoded by PyTorch (not the oracle's table) and the final
+    rounding by exact_fp8."""
+    xs = gen.rank_inputs(n, 96, fmt, dist, seed_base=311 + n)
+    scale = 0.25 if n > 2 else 1.0
+    got = O.fold_ascending(xs, scale=scale)
+    assert O.fp8_format(got.dtype) == fmt
+    cols = list(zip(*[_torch_fp8_values(x, tname).tolist() for x in xs]))
+    want = []
+    for vals in cols:
+        acc = float(vals[0])
+        for v in vals[1:]:
+            acc = exact_add(acc, float(v))
+        want.append(exact_fp8(exact_mul(acc, scale), fmt))
+    assert _same_f32(O.widen(got), want)
+
+
+@pytest.mark.parametrize("fmt,tname", FP8_FORMATS)
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("algo", ["flat", "dbt", "pair_dbt"])
+def test_integer_closed_form_fp8(fmt, tname, n, algo):
+    """|x| <= 8, n <= 8: every fp32 partial sum is an exact integer (<= 64) in
+    any order, so every schedule gives RNE_fp8(integer sum) — computed here by
+    PyTorch's conversion of the int64 sum."""
+    import torch
+    xs = gen.rank_inputs(n, 3000, fmt, "int", seed_base=17)
+    ints = [_torch_fp8_values(x, tname).astype(np.int64) for x in xs]
+    total = sum(ints)
+    want = torch.from_numpy(total.astype(np.float32)).to(getattr(torch, tname)).view(torch.uint8).numpy()
+    got = O.allreduce(xs, algo, chunk_elems=256)[0]
+    assert np.array_equal(got.view(np.uint8), want)
