@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-nccl", action="store_true")
     p.add_argument("--no-variants", action="store_true")
+    p.add_argument("--no-probe", action="store_true", help="skip the NVLink probe (roofline peak falls back)")
+    p.add_argument("--no-nvls", action="store_true", help="no NVLS arena (plain symmetric memory)")
     p.add_argument("--e2e-chunks", type=int, default=8, help="pipeline depth of the e2e step (1 = sequential)")
     return p.parse_args()
 
@@ -382,17 +384,20 @@ def main():
     probe = None
     if multi:
         # the per-direction NVLink peak of this lease, before anything else runs
-        if rank == 0:
+        if rank == 0 and not args.no_probe:
             probe = nvlink_probe(n)
         dist.barrier()
     nvls_note = None
-    if multi:
+    if multi and not args.no_nvls:
         # NVLS arena (order-relaxed variant) holds the bench buffer; FLAT runs on it zero-copy too
         try:
             comm = hfr.Comm.init(device=local, config=hfr.Config(**{**cfg.__dict__, "nvls_bytes": S + (64 << 20)}))
         except hfr.HfrError as e:
             nvls_note = f"no NVLS arena: {e}"
             comm = hfr.Comm.init(device=local, config=cfg)
+    elif multi:
+        nvls_note = "no NVLS arena (--no-nvls)"
+        comm = hfr.Comm.init(device=local, config=cfg)
     else:
         comm = hfr.Comm.virtual_ranks(n, local, cfg)
     stream = torch.cuda.current_stream()

@@ -28,8 +28,13 @@ def test_multiprocess_parity_protocol_timeout(tmp_path):
     from tests import mp_worker
     world = min(torch.cuda.device_count(), 8)
     mp.spawn(mp_worker.entry, args=(world, _free_port(), str(tmp_path), "gpu"), nprocs=world, join=True)
+    keep = os.environ.get("HFR_MULTI_OUT")  # copy the per-rank verdicts out (profiles/ evidence)
     for r in range(world):
         res = json.load(open(os.path.join(tmp_path, f"rank{r}.json")))
+        if keep:
+            os.makedirs(keep, exist_ok=True)
+            with open(os.path.join(keep, f"multigpu_n{world}_rank{r}.json"), "w") as f:
+                json.dump(res, f, indent=0)
         assert not res["fail"], res["fail"]
         assert "protocol" in res["ok"] and "ddp" in res["ok"] and "1gib" in res["ok"] and "ddp-tail-1" in res["ok"]
         assert "protocol-grid-flat" in res["ok"] and "protocol-grid-auto" in res["ok"]
