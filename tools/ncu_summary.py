@@ -5,8 +5,9 @@
 
 For each --set full report: key raw metrics (duration, DRAM bytes, throughput,
 occupancy, registers) and the stall-reason breakdown -> profiles/<tag>_<name>.txt,
-and the per-launch DRAM traffic -> profiles/traffic.json (read by bench.py for
-roofline.traffic).  For a launch list: per-kernel count / total / share.
+For a launch list: per-kernel count / total / share.  (Per-launch traffic for
+bench.py's roofline.traffic is recorded by tools/traffic_record.py, tied to
+the source hash of the profiled build.)
 """
 from __future__ import annotations
 
@@ -72,10 +73,8 @@ def main():
         launches = args[i + 1]
         del args[i:i + 2]
     os.makedirs(PROF, exist_ok=True)
-    tpath = os.path.join(PROF, "traffic.json")
-    traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for spec in args:
-        rep, _, key = spec.partition("=")
+        rep = spec.partition("=")[0]
         name = os.path.basename(rep).replace(".ncu-rep", "")
         lines = [f"# ncu --set full summary: {rep} ({tag})"]
         for d in raw(rep):
@@ -86,8 +85,6 @@ def main():
             rd, wr = si(d.get("dram__bytes_read.sum", ("", ""))), si(d.get("dram__bytes_write.sum", ("", "")))
             if rd is not None and wr is not None:
                 lines.append(f"  dram read+write per launch: {rd + wr:.4e} B")
-                if key:
-                    traffic[key] = rd + wr
         lines.append("")
         lines.append(stalls(rep))
         open(os.path.join(PROF, f"{tag}_{name}.txt"), "w").write("\n".join(lines) + "\n")
@@ -108,7 +105,6 @@ def main():
             out.append(f"{k[:60]:60s} {len(v):8d} {sum(v) / 1e3:12.1f} {sum(v) / len(v) / 1e3:10.1f} {sum(v) / tot:7.1%}")
         open(os.path.join(PROF, f"{tag}_launches.txt"), "w").write("\n".join(out) + "\n")
         print("\n".join(out))
-    json.dump(traffic, open(tpath, "w"), indent=1)
 
 
 if __name__ == "__main__":
