@@ -23,7 +23,7 @@ namespace hfr {
 
 constexpr int kMaxRanks = 16;
 constexpr int kMaxCtas = 1024;
-constexpr int kMaxChunks = 65536;
+constexpr int kMaxChunks = 1 << 18;  // tree flags per launch (chunks, or tiles for the TMA tree kernel)
 
 // Peer-mapped signal pad, one per rank (DESIGN.md §5 "HBM layout").
 // entry/exit[b][q] are written by rank q's CTA b; up/down/pdown[c] are the
@@ -88,6 +88,8 @@ struct Args {
   uint32_t* uc_exit;       // NVLS: local unicast VA of the same counters
   uint32_t trace_cap;      // diagnostic trace: events per CTA (0 = off)
   uint64_t* trace;         // [local rank][CTA][trace_cap][4] u64, see Tracer
+  uint32_t tree_tile;      // TMA tree kernel: elements per tile (flag granularity), divides chunk
+  int tree_stages;         // TMA tree kernel: shared-memory stages
   TreeNode tree[2][kMaxRanks];
 };
 

@@ -23,6 +23,7 @@
 
 #include "../../include/hfr.h"
 #include "hfr_kernels.cuh"
+#include "hfr_tree_tma.cuh"
 
 using namespace hfr;
 
@@ -264,6 +265,7 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
   if (c.stream_gate != 0 && c.stream_gate != 1) return HFR_ERR_INVALID_ARGUMENT;
   if (c.flat_staging < 0 || c.flat_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   if (c.pdl_off != 0 && c.pdl_off != 1) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.tree_staging < 0 || c.tree_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   return HFR_SUCCESS;
 }
 
@@ -698,18 +700,26 @@ hfr_status_t run_flat(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   return launch(c, fn, g, threads, a, s);
 }
 
+template <class E>
+const void* tree_tma_fn(bool pair) {
+  return pair ? (const void*)hfr_tree_tma_kernel<E, true> : (const void*)hfr_tree_tma_kernel<E, false>;
+}
+
+// TMA tree kernel geometry: tile = the largest power of two dividing the
+// chunk, at most 2048 elements, halved until a stage fits 36 KiB (so three
+// stages leave room for 2 CTAs per SM); hfr_tree_tma.cuh TreeStage.
+constexpr int kTreeStages = 3;
+uint32_t tree_stage_bytes(uint32_t T, uint32_t esz, bool pair) { return T * esz * (pair ? 2 : 1) + 12 * T; }
+uint32_t tree_tile(uint64_t C, uint32_t esz, bool pair) {
+  uint32_t T = 2048;
+  while (C % T) T >>= 1;
+  while (T > 256 && tree_stage_bytes(T, esz, pair) > (36u << 10)) T >>= 1;
+  return T;
+}
+
 hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, bool pair, uint64_t sig,
                       cudaStream_t s, size_t area) {
-#define HFR_TREE_FN(E) tree_fn<E>(pair)
-  const void* fn = HFR_BY_DTYPE(dt, HFR_TREE_FN);
-  // 2-3 CTAs x 256 threads per SM: while one CTA drains its chunk's stores
-  // at the per-chunk system fence the others issue (r01, n=4: DBT 1 -> 2
-  // CTAs/SM 377 -> 422 GB/s; fp32 DBT 2 -> 3 CTAs/SM 423 -> 442 and n=2
-  // 572 -> 591, but PAIR (shared-memory partner ring) 590-609 -> 561 and
-  // bf16 DBT 388 -> 377, so those keep 2)
-  const int threads = cta_threads(c, 256);
   const uint64_t C = tree_chunk(c);
-  const int per_sm = !pair && dt == HFR_FLOAT32 ? 3 : 2;
   Args a;
   base_args(c, a, count, 0);
   if (pair) {
@@ -732,6 +742,59 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
     a.buf[q] = bufs[q];
     a.part[q] = reinterpret_cast<float*>(stage_base(c, q) + area);
   }
+  const bool tma = c->cfg.tree_staging != 1;
+  if (tma) {
+    // hfr_tree_tma.cuh: one producer thread + 3 fold warps per CTA, flags per
+    // tile, 3-stage shared-memory ring.  All CTAs of every rank must be
+    // co-resident (a CTA spins on tiles of peers' CTAs), so the grid is capped
+    // by the occupancy at this shared-memory size.
+#define HFR_TREE_TMA_FN(E) tree_tma_fn<E>(pair)
+    const void* fn = HFR_BY_DTYPE(dt, HFR_TREE_TMA_FN);
+    const uint32_t esz = (uint32_t)dtype_size(dt);
+    const uint32_t T = tree_tile(C, esz, pair);
+    const int smem = kTreeStages * (int)tree_stage_bytes(T, esz, pair);
+    static std::vector<std::pair<const void*, int>> smem_set;
+    if (std::find(smem_set.begin(), smem_set.end(), std::make_pair(fn, smem)) == smem_set.end()) {
+      HFR_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      smem_set.emplace_back(fn, smem);
+    }
+    int occ = 0;
+    HFR_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTreeThreads, smem));
+    if (occ < 1) return HFR_ERR_UNSUPPORTED;
+    const int per_sm = std::min(occ, 2);
+    a.tree_tile = T;
+    a.tree_stages = kTreeStages;
+    const uint64_t nt = (a.half_len[0] + T - 1) / T;  // tiles of the longer half
+    for (uint64_t lo = 0; lo < std::max<uint64_t>(nt, 1); lo += kMaxChunks) {
+      const uint64_t hi = lo + kMaxChunks;
+      const uint64_t here = std::min<uint64_t>(nt, hi) - std::min<uint64_t>(nt, lo);
+      int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : per_sm * c->num_sms;
+      g = std::min(g, occ * c->num_sms / c->local);
+      g = (int)std::min<uint64_t>((uint64_t)g, std::max<uint64_t>(here, 2));
+      g = std::max(2, std::min(g, kMaxCtas) & ~1);  // even: CTA b works on tree b & 1 only
+      a.c_lo = (uint32_t)lo;
+      a.c_hi = (uint32_t)hi;
+      a.sig = fnv(fnv(fnv(sig, (uint64_t)g * 1315423911ull + kTreeThreads), lo), 0x7474ull + T * 16 + kTreeStages);
+      ++c->epoch;
+      void* params[] = {&a};
+      const cudaError_t e = launch_protocol_kernel(c, fn, dim3(g, c->local), dim3(kTreeThreads), params, smem, s, false);
+      if (e != cudaSuccess) {
+        note_cuda(e, "hfr_tree_tma_kernel");
+        return HFR_ERR_CUDA;
+      }
+      ++c->launches;
+    }
+    return HFR_SUCCESS;
+  }
+#define HFR_TREE_FN(E) tree_fn<E>(pair)
+  const void* fn = HFR_BY_DTYPE(dt, HFR_TREE_FN);
+  // register staging: 2-3 CTAs x 256 threads per SM: while one CTA drains its
+  // chunk's stores at the per-chunk system fence the others issue (r01, n=4:
+  // DBT 1 -> 2 CTAs/SM 377 -> 422 GB/s; fp32 DBT 2 -> 3 CTAs/SM 423 -> 442 and
+  // n=2 572 -> 591, but PAIR (shared-memory partner ring) 590-609 -> 561 and
+  // bf16 DBT 388 -> 377, so those keep 2)
+  const int threads = cta_threads(c, 256);
+  const int per_sm = !pair && dt == HFR_FLOAT32 ? 3 : 2;
   const uint64_t nch = (a.half_len[0] + C - 1) / C;  // half 0 is the longer one
   for (uint64_t lo = 0; lo < std::max<uint64_t>(nch, 1); lo += kMaxChunks) {
     const uint64_t hi = lo + kMaxChunks;

@@ -385,3 +385,48 @@ def test_collectives_fp8(hfr, n, dtype, kind):
             "reduce": lambda: O.reduce(xs, 1, 0.5), "broadcast": lambda: O.broadcast(xs, 1)}[kind]()
     for r, b in enumerate(bufs):
         assert_bit_exact(to_numpy(b), want[r], f"{kind} fp8 n={n} rank {r}")
+
+
+def run_cfg(hfr, n, xs, cfg):
+    """run() with an explicit Config (the tree kernels' staging modes)."""
+    comm = comm_for(hfr, n)
+    comm.set_config(cfg)
+    N = xs[0].shape[0]
+    bufs = comm.empty(N, torch_dtype(dtype_of(xs[0])))
+    for b, x in zip(bufs, xs):
+        b.copy_(to_torch(x, "cuda:0"))
+    comm.allreduce_virtual(bufs)
+    torch.cuda.synchronize()
+    assert comm.status() == hfr.SUCCESS, hfr.status_string(comm.status())
+    return [to_numpy(b) for b in bufs]
+
+
+@pytest.mark.parametrize("staging", [1, 2])
+@pytest.mark.parametrize("algo", ["dbt", "pair_dbt"])
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16, gen.E4M3])
+@pytest.mark.parametrize("chunk,N", [(4096, 300_007), (8192, 1_000_003), (24576, 123_457), (256, 4096 + 13)])
+def test_tree_staging_modes(hfr, staging, algo, n, dtype, chunk, N):
+    """Both tree data paths (1: SM loads/stores + per-chunk fence; 2: TMA bulk
+    copies with per-tile flags, several tiles per chunk when chunk > 2048)
+    give the tree-order oracle's bits, incl. ragged half ends."""
+    if algo == "pair_dbt" and n % 2:
+        pytest.skip("pair-first needs even n")
+    xs = gen.rank_inputs(n, N, dtype, "normal", seed_base=3300 + N)
+    outs = run_cfg(hfr, n, xs, hfr.Config(algo=algo, chunk_elems=chunk, scale=0.25, tree_staging=staging))
+    check(outs, O.allreduce(xs, algo, chunk_elems=chunk, scale=0.25)[0], f"{algo} staging={staging} n={n}")
+
+
+@pytest.mark.parametrize("algo", ["dbt", "pair_dbt"])
+def test_tree_many_tiles_segments(hfr, algo):
+    """More tiles than one launch's flag array (2^18): the schedule splits
+    into several launches (segments) — bf16, n=2, 256-element chunks."""
+    n, N = 2, (1 << 18) * 256 * (2 if algo == "pair_dbt" else 1) + 1001
+    xs = gen.rank_inputs(n, N, gen.BF16, "normal", seed_base=12)
+    comm = comm_for(hfr, n)
+    launches = comm.launches
+    outs = run_cfg(hfr, n, xs, hfr.Config(algo=algo, chunk_elems=256, scale=0.5))
+    assert comm.launches - launches >= 2
+    check(outs, O.allreduce(xs, algo, chunk_elems=256, scale=0.5)[0], f"{algo} segments")
+    del outs
+    comm.free_all()
