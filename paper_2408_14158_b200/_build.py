@@ -27,14 +27,13 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
-    """Build libhfr.so, or an experimental variant libhfr_<variant>.so with
-    -DHFR_VARIANT_<VARIANT>=1 (selected at run time with HFR_LIB=<path>)."""
-    lib = LIB if not variant else LIB.replace("libhfr.so", f"libhfr_{variant}.so")
-    defs = [f"-DHFR_VARIANT_{variant.upper()}=1"] if variant else []
-    if force or variant or stale():
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Build libhfr.so in-tree (one library, no variants: every behaviour
+    switch is a field of hfr_config_t)."""
+    lib = LIB
+    if force or stale():
         tmp = lib + f".tmp{os.getpid()}"
-        cmd = [NVCC, *FLAGS, *defs, "-o", tmp, *SRC]
+        cmd = [NVCC, *FLAGS, "-o", tmp, *SRC]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -48,5 +47,4 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
 
 
 if __name__ == "__main__":
-    variant = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--variant=")), "")
-    print(build(force=True, verbose="-v" in sys.argv, variant=variant))
+    print(build(force=True, verbose="-v" in sys.argv))

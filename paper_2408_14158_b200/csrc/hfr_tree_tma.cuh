@@ -309,48 +309,57 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
         }
       }
     };
+    // Event loop.  Every blocking wait here is CTA-local (bulk loads, fold
+    // warps, bulk-store completion); dependencies on other ranks are polled,
+    // and while the CTA is held up by them every completed tile is retired, so
+    // a flag a peer waits for is never held back.
+    uint32_t idle = 0;
     while (retired < NJ) {
       bool did = false;
-      // (A) load the next job once its stage is free and its dependencies landed
-      if (loaded < NJ && loaded < retired + S) {
+      // (A) loads, as far as the stages and the polled dependencies allow
+      while (loaded < NJ && loaded < retired + S) {
         const uint32_t st = (uint32_t)(loaded % S);
-        if (loaded >= S) mbar_wait(&done[st], (uint32_t)((loaded / S - 1) & 1));  // local: consumers
+        if (loaded >= S && !mbar_test(&done[st], (uint32_t)((loaded / S - 1) & 1))) break;  // fold warps still on it
         const Job J = job(loaded);
         if (tr.p && !t_poll) t_poll = globaltimer();
-        if (deps_ready(J)) {
-          if (tr.p) {
-            tq[st][0] = t_poll;
-            tq[st][1] = globaltimer();
-          }
-          t_poll = 0;
-          issue_loads(J, st);
-          ++loaded;
-          did = true;
+        if (!deps_ready(J)) break;
+        if (tr.p) {
+          tq[st][0] = t_poll;
+          tq[st][1] = globaltimer();
         }
+        t_poll = 0;
+        issue_loads(J, st);
+        ++loaded;
+        did = true;
       }
-      // (B) store the next loaded job (waits are local: bulk loads, fold warps)
+      // (B) stores of the next job once its stage is ready
+      bool stalled = true;
       if (stored < loaded) {
         const uint32_t st = (uint32_t)(stored % S);
         const uint32_t ph = (uint32_t)((stored / S) & 1);
         const Job J = job(stored);
-        mbar_wait(is_compute(J) ? &done[st] : &full[st], ph);
-        issue_stores(J, st);
-        bulk_commit();
-        if (tr.p) tq[st][2] = globaltimer();
-        ++stored;
-        did = true;
-        if (stored - retired > 1) {  // keep the newest group in flight, retire the older ones
-          bulk_wait_1();
-          retire_to(stored - 1);
+        if (mbar_test(is_compute(J) ? &done[st] : &full[st], ph)) {
+          issue_stores(J, st);
+          bulk_commit();
+          if (tr.p) tq[st][2] = globaltimer();
+          ++stored;
+          did = true;
+          if (stored - retired > 1) {  // keep the newest group in flight, retire the older ones
+            bulk_wait_1();
+            retire_to(stored - 1);
+          }
         }
-      } else if (retired < stored) {  // nothing else can move: drain
+        stalled = false;  // a loaded job will become ready without any peer
+      }
+      if (stalled && retired < stored) {  // held up by peers only: release everything
         bulk_wait_0();
         retire_to(stored);
         did = true;
       }
       if (did) {
+        idle = 0;
         t_idle = 0;
-      } else {
+      } else if ((++idle & 63u) == 0) {
         const uint64_t now = globaltimer();
         if (!t_idle) t_idle = now;
         if (*a.err != 0) abort = true;
