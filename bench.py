@@ -60,6 +60,9 @@ def parse():
     p.add_argument("--no-variants", action="store_true")
     p.add_argument("--no-probe", action="store_true", help="skip the NVLink probe (roofline peak falls back)")
     p.add_argument("--no-nvls", action="store_true", help="no NVLS arena (plain symmetric memory)")
+    p.add_argument("--dist", default="nccl", choices=["nccl", "gloo"],
+                   help="torch.distributed backend for the host plumbing (gloo under ncu: no NCCL kernels; "
+                        "implies --no-nccl)")
     p.add_argument("--e2e-chunks", type=int, default=8, help="pipeline depth of the e2e step (1 = sequential)")
     return p.parse_args()
 
@@ -371,7 +374,11 @@ def main():
     dev = torch.device("cuda", local)
     multi = world > 1
     if multi:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist == "gloo":
+            dist.init_process_group("gloo")
+            args.no_nccl = True
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     dtype = args.dtype
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
     esz = 2 if dtype == "bf16" else 4
@@ -424,7 +431,7 @@ def main():
     def max_over_ranks(v: float) -> float:
         if not multi:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=dev if args.dist == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

@@ -11,3 +11,10 @@ timeout 600 $R --master-port 29632 tools/sweep.py --algos dbt,pair_dbt --tree-st
 timeout 600 $R --master-port 29633 tools/sweep.py --dtype bf16 --algos dbt,pair_dbt --tree-staging 1,2 --sizes 1073741824,67108864,8388608 --out gpurun_out/r02e_trees_bf16_n2.jsonl > gpurun_out/r02e_sweep3.log 2>&1; echo sweep3=$?
 timeout 1500 python -m pytest tests -m gpu -q -rs --durations=10 > gpurun_out/r02e_gpu_tests.log 2>&1; echo tests=$?
 tail -15 gpurun_out/r02e_gpu_tests.log
+# ncu NVLink/DRAM bytes of one FLAT-TMA launch at n=2, host plumbing over gloo (no NCCL kernels under ncu)
+BN="bench.py --gpus 2 --steps 4 --warmup 3 --no-cpu --no-e2e --no-variants --no-probe --no-nvls --soak 0 --dist gloo"
+python -c "import bench; print(bench.source_sha())" > gpurun_out/r02e_source_sha.txt
+timeout 240 $R --master-port 29634 --no-python bash tools/ncu_rank0.sh gpurun_out/r02e_nvl_n2.csv nvltx__bytes.sum,nvlrx__bytes.sum hfr_flat_tma 5 $BN > gpurun_out/r02e_ncu_nvl_n2.log 2>&1; echo nvl=$?
+tail -4 gpurun_out/r02e_ncu_nvl_n2.log; cat gpurun_out/r02e_nvl_n2.csv
+timeout 240 $R --master-port 29635 --no-python bash tools/ncu_rank0.sh gpurun_out/r02e_dram_n2.csv dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum hfr_flat_tma 5 $BN > gpurun_out/r02e_ncu_dram_n2.log 2>&1; echo dram=$?
+cat gpurun_out/r02e_dram_n2.csv
