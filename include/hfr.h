@@ -152,6 +152,7 @@ typedef struct {
                              one flag and one system fence per chunk), 2 TMA (bulk copies in and out of
                              shared memory, one flag per tile of <= 2048 elements, raised when the
                              tile's bulk stores completed).  Bits are identical either way. */
+    int tree_sync;        /* EXPERIMENT (round 2, to be removed): TMA tree fence variant bits */
 } hfr_config_t;
 
 /* Fill *cfg with the defaults above (algo AUTO, scale 1.0). */

@@ -90,6 +90,7 @@ struct Args {
   uint64_t* trace;         // [local rank][CTA][trace_cap][4] u64, see Tracer
   uint32_t tree_tile;      // TMA tree kernel: elements per tile (flag granularity), divides chunk
   int tree_stages;         // TMA tree kernel: shared-memory stages
+  int tree_sync;           // TMA tree kernel, experiment: fence variant (0 = full)
   TreeNode tree[2][kMaxRanks];
 };
 
@@ -106,13 +107,16 @@ struct Tracer {
       p = a.trace + ((uint64_t)blockIdx.y * kMaxCtas + blockIdx.x) * cap * 8;
     }
   }
-  __device__ __forceinline__ void rec(uint64_t tag, uint64_t t0, uint64_t t1, uint64_t t2, uint64_t t3) {
+  __device__ __forceinline__ void rec(uint64_t tag, uint64_t t0, uint64_t t1, uint64_t t2, uint64_t t3,
+                                      uint64_t t4 = 0, uint64_t t5 = 0) {
     if (p && n < cap) {
       p[8 * n] = tag;
       p[8 * n + 1] = t0;
       p[8 * n + 2] = t1;
       p[8 * n + 3] = t2;
       p[8 * n + 4] = t3;
+      p[8 * n + 5] = t4;
+      p[8 * n + 6] = t5;
       ++n;
     }
   }

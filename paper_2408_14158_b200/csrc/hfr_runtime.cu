@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -266,6 +267,7 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
   if (c.flat_staging < 0 || c.flat_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   if (c.pdl_off != 0 && c.pdl_off != 1) return HFR_ERR_INVALID_ARGUMENT;
   if (c.tree_staging < 0 || c.tree_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.tree_sync < 0 || c.tree_sync > 7) return HFR_ERR_INVALID_ARGUMENT;
   return HFR_SUCCESS;
 }
 
@@ -631,6 +633,26 @@ void coll_routing(const hfr_comm_s* c, int coll, int root, int* src, uint32_t* d
   }
 }
 
+// The kernel attribute is a per-function MAXIMUM: raise it to the largest
+// dynamic shared memory asked for so far, never lower it (a lower value set
+// for a smaller call would make a later, larger launch of the same kernel
+// fail or report zero occupancy).
+hfr_status_t allow_dynamic_smem(const void* fn, int smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> set;  // (kernel, bytes allowed)
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : set)
+    if (e.first == fn) {
+      if (smem <= e.second) return HFR_SUCCESS;
+      HFR_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      e.second = smem;
+      return HFR_SUCCESS;
+    }
+  HFR_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  set.emplace_back(fn, smem);
+  return HFR_SUCCESS;
+}
+
 // TMA-staged FLAT (default for allreduce / reduce-scatter / reduce with n in {2, 4, 8})
 hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, uint64_t sig,
                           cudaStream_t s, int coll, int root, const void* fn) {
@@ -643,11 +665,7 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
   const int per_sm = c->virt && c->local > 1 ? 2 : 1;
   const int threads = cta_threads(c, 256);
   const int smem = 2 * c->n * tile;
-  static std::vector<std::pair<const void*, int>> smem_set;  // (kernel, bytes) already configured
-  if (std::find(smem_set.begin(), smem_set.end(), std::make_pair(fn, smem)) == smem_set.end()) {
-    HFR_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    smem_set.emplace_back(fn, smem);
-  }
+  HFR_TRY(allow_dynamic_smem(fn, smem));
   int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : per_sm * c->num_sms;
   // no more CTAs than tiles: idle CTAs would only add handshakes
   const uint64_t per = per_vec(dt);
@@ -753,17 +771,14 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
     const uint32_t esz = (uint32_t)dtype_size(dt);
     const uint32_t T = tree_tile(C, esz, pair);
     const int smem = kTreeStages * (int)tree_stage_bytes(T, esz, pair);
-    static std::vector<std::pair<const void*, int>> smem_set;
-    if (std::find(smem_set.begin(), smem_set.end(), std::make_pair(fn, smem)) == smem_set.end()) {
-      HFR_CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      smem_set.emplace_back(fn, smem);
-    }
+    HFR_TRY(allow_dynamic_smem(fn, smem));
     int occ = 0;
     HFR_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTreeThreads, smem));
     if (occ < 1) return HFR_ERR_UNSUPPORTED;
     const int per_sm = std::min(occ, 2);
     a.tree_tile = T;
     a.tree_stages = kTreeStages;
+    a.tree_sync = c->cfg.tree_sync;
     const uint64_t nt = (a.half_len[0] + T - 1) / T;  // tiles of the longer half
     for (uint64_t lo = 0; lo < std::max<uint64_t>(nt, 1); lo += kMaxChunks) {
       const uint64_t hi = lo + kMaxChunks;

@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
       }
       mbar_expect_tx(&full[st], tx);
       if (!J.Lv) return;
-      fence_proxy_global();  // the acquired flags before the bulk reads
+      if (!(a.tree_sync & 1)) fence_proxy_global();  // the acquired flags before the bulk reads
       bulk_g2s(sb + G.X, a.buf[rank] + xb, xbytes, &full[st]);
       if (J.down) return;
       if (PAIR) bulk_g2s(sb + G.P, a.buf[partner] + xb, xbytes, &full[st]);
@@ -296,16 +296,17 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
       }
     };
     // retire jobs [retired, upto): their bulk groups are complete
-    auto retire_to = [&](uint64_t upto) {
-      fence_proxy_global();
-      fence_acq_rel_sys();  // ... and the remainder's plain stores
+    auto retire_to = [&](uint64_t upto, uint64_t t_waited) {
+      if (!(a.tree_sync & 2)) fence_proxy_global();
+      if (!(a.tree_sync & 4)) fence_acq_rel_sys();  // ... and the remainder's plain stores
+      const uint64_t t_fenced = tr.p ? globaltimer() : 0;
       for (; retired < upto; ++retired) {
         const Job J = job(retired);
         raise(J);
         if (tr.p) {
           const uint32_t st = (uint32_t)(retired % S);
           tr.rec(((J.down ? 2ull : 1ull) << 60) | ((uint64_t)rank << 48) | J.t, tq[st][0], tq[st][1], tq[st][2],
-                 globaltimer());
+                 globaltimer(), t_waited, t_fenced);
         }
       }
     };
@@ -346,14 +347,14 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
           did = true;
           if (stored - retired > 1) {  // keep the newest group in flight, retire the older ones
             bulk_wait_1();
-            retire_to(stored - 1);
+            retire_to(stored - 1, tr.p ? globaltimer() : 0);
           }
         }
         stalled = false;  // a loaded job will become ready without any peer
       }
       if (stalled && retired < stored) {  // held up by peers only: release everything
         bulk_wait_0();
-        retire_to(stored);
+        retire_to(stored, tr.p ? globaltimer() : 0);
         did = true;
       }
       if (did) {

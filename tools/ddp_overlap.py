@@ -87,7 +87,10 @@ def main():
     nvls = (TOTAL * 2 + (256 << 20)) if a.algo == "nvls" else 0
     cfg = hfr.Config(algo=a.algo, max_ctas=a.max_ctas, scale=1.0 / world, stream_gate=a.gate, nvls_bytes=nvls,
                      threads=a.threads, flat_staging=a.staging)
-    comm = hfr.Comm.init(device=local, config=cfg)
+    # the comm's own config is the full-width default (T_comm_full); the DDP
+    # buckets that overlap the backward use `cfg`
+    comm = hfr.Comm.init(device=local, config=hfr.Config(algo=a.algo, scale=1.0 / world, stream_gate=a.gate,
+                                                         nvls_bytes=nvls))
     tail_cfg = hfr.Config(algo=a.tail_algo, scale=1.0 / world, stream_gate=a.gate) if a.tail else None
     tail_from = [nm for nm, _, _ in params].index("embed")
     ddp = HaiScaleDDP(comm, numels, torch.bfloat16, bucket_bytes=a.bucket_mib << 20, config=cfg,
@@ -119,6 +122,15 @@ def main():
             ddp.mark_ready(idx, compute)
         ddp.finish(compute)
 
+    def comm_full():
+        """every bucket with the comm's full-width default config"""
+        keep = ddp.config, ddp.tail_config
+        ddp.config = ddp.tail_config = None
+        try:
+            comm_only()
+        finally:
+            ddp.config, ddp.tail_config = keep
+
     def timed(fn):
         dist.barrier()
         comm.barrier(compute)
@@ -135,18 +147,19 @@ def main():
     backward(True)  # warm-up (cuBLAS heuristics, IPC mappings)
     comm_only()
     from bench import Clocks
-    res = {"bwd": [], "comm": [], "both": []}
+    res = {"bwd": [], "comm": [], "both": [], "comm_full": []}
     # interleaved repetitions (bwd, comm, both, bwd, ...) so slow drifts of the
     # power-capped clock hit all three alike; overlap also reported per rep
     ck = Clocks(local, interval_ms=20)
     ck.start()
     for _ in range(a.reps):
-        for name, fn in (("bwd", lambda: backward(False)), ("comm", comm_only), ("both", lambda: backward(True))):
+        for name, fn in (("bwd", lambda: backward(False)), ("comm", comm_only), ("both", lambda: backward(True)),
+                         ("comm_full", comm_full)):
             res[name].append(timed(fn))
     clk = {"all": ck.stop()}
     if comm.status() != hfr.SUCCESS:
         raise SystemExit(hfr.status_string(comm.status()))
-    tb, tc, tt = (statistics.median(res[k]) for k in ("bwd", "comm", "both"))
+    tb, tc, tt, tf = (statistics.median(res[k]) for k in ("bwd", "comm", "both", "comm_full"))
     S = ddp.total * 2
     n = world
     flops = sum(4 * T * o * i for _, o, i in params if o > 1 and i <= 65536)
@@ -157,6 +170,9 @@ def main():
             "stream_gate": a.gate, "threads": a.threads, "flat_staging": a.staging, "side_priority": os.environ.get("HFR_SIDE_PRIORITY", "high"),
             "tokens": T, "T_bwd_ms": tb * 1e3, "T_comm_ms": tc * 1e3, "T_both_ms": tt * 1e3,
             "overlap": (tb + tc - tt) / tc, "bwd_slowdown": tt / tb,
+            "T_comm_full_ms": tf * 1e3,
+            # against the full-width allreduce time: 1 - exposed / T_comm_full
+            "overlap_vs_full": 1.0 - (tt - tb) / tf, "comm_full_busbw": S / tf * 2 * (n - 1) / n / 1e9,
             "overlap_paired_median": statistics.median((b + c - t) / c for b, c, t in zip(res["bwd"], res["comm"],
                                                                                             res["both"])),
             "overlap_min": (min(res["bwd"]) + min(res["comm"]) - min(res["both"])) / min(res["comm"]),

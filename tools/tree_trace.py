@@ -49,6 +49,10 @@ def analyze(d):
                          "issue_us_mean": float((ts[m] - t1[m]).mean() / 1e3),
                          "drain_us_mean": float((t2[m] - ts[m]).mean() / 1e3),
                          "first_done_us": float((t2[m].min() - base) / 1e3),
+                         # TMA tree kernel only (slots 5/6: bulk-group wait done, fences done)
+                         **({"bulk_wait_us_mean": float((ev[m, 5].astype(np.int64) - ts[m]).mean() / 1e3),
+                             "fence_us_mean": float((ev[m, 6].astype(np.int64) - ev[m, 5].astype(np.int64)).mean() / 1e3)}
+                            if (ev[m, 5] != 0).all() else {}),
                          "last_done_us": float((t2[m].max() - base) / 1e3)}
         # per-CTA busy fraction
         ctas = tr.shape[0]
@@ -72,6 +76,8 @@ def main():
     ap.add_argument("--ctas", type=int, default=64)
     ap.add_argument("--bytes", type=int, default=186 << 20)
     ap.add_argument("--out", default="gpurun_out/trace")
+    ap.add_argument("--staging", type=int, default=0, help="hfr_config.tree_staging")
+    ap.add_argument("--sync", type=int, default=0, help="hfr_config.tree_sync (experiment)")
     a = ap.parse_args()
     if a.analyze:
         print(json.dumps(analyze(a.analyze), indent=1))
@@ -87,7 +93,8 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comm = hfr.Comm.init(device=local, config=hfr.Config(algo=a.algo, chunk_elems=a.chunk, max_ctas=a.ctas,
-                                                        scale=1.0 / dist.get_world_size()))
+                                                        scale=1.0 / dist.get_world_size(),
+                                                        tree_staging=a.staging, tree_sync=a.sync))
     t = comm.empty(a.bytes // 4, torch.float32)
     t.normal_()
     for _ in range(3):
@@ -110,7 +117,8 @@ def main():
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     if rank == 0:
         n = dist.get_world_size()
-        print(json.dumps({"algo": a.algo, "chunk": a.chunk, "ctas": a.ctas, "n": n, "ms": float(ms),
+        print(json.dumps({"algo": a.algo, "chunk": a.chunk, "ctas": a.ctas, "staging": a.staging, "sync": a.sync,
+                          "n": n, "ms": float(ms),
                           "busbw": a.bytes / (float(ms) / 1e3) * 2 * (n - 1) / n / 1e9}))
     comm.finalize()
     dist.destroy_process_group()
