@@ -89,8 +89,8 @@ struct Args {
   uint32_t trace_cap;      // diagnostic trace: events per CTA (0 = off)
   uint64_t* trace;         // [local rank][CTA][trace_cap][4] u64, see Tracer
   uint32_t tree_tile;      // TMA tree kernel: elements per tile (flag granularity), divides chunk
-  int tree_stages;         // TMA tree kernel: shared-memory stages
-  int tree_sync;           // TMA tree kernel, experiment: fence variant (0 = full)
+  int tree_smem;           // TMA tree kernel: dynamic shared memory per CTA (each role fits its own stages)
+  int tree_sync;           // TMA tree kernel, experiment: fence variant bits (0 = default)
   TreeNode tree[2][kMaxRanks];
 };
 

@@ -723,15 +723,17 @@ const void* tree_tma_fn(bool pair) {
   return pair ? (const void*)hfr_tree_tma_kernel<E, true> : (const void*)hfr_tree_tma_kernel<E, false>;
 }
 
-// TMA tree kernel geometry: tile = the largest power of two dividing the
-// chunk, at most 2048 elements, halved until a stage fits 36 KiB (so three
-// stages leave room for 2 CTAs per SM); hfr_tree_tma.cuh TreeStage.
-constexpr int kTreeStages = 3;
-uint32_t tree_stage_bytes(uint32_t T, uint32_t esz, bool pair) { return T * esz * (pair ? 2 : 1) + 12 * T; }
+// TMA tree kernel geometry (hfr_tree_tma.cuh TreeStage): a 100 KiB
+// shared-memory budget per CTA (2 CTAs per SM); the tile is the largest power
+// of two dividing the chunk, at most 2048 elements, halved until the largest
+// role's stage (x, partner x, two fp32 child partials, fp32 output) fits a
+// third of the budget, so every role gets >= 3 stages.
+constexpr int kTreeSmem = 100 << 10;
+uint32_t tree_stage_max(uint32_t T, uint32_t esz, bool pair) { return T * esz * (pair ? 2 : 1) + 12 * T; }
 uint32_t tree_tile(uint64_t C, uint32_t esz, bool pair) {
   uint32_t T = 2048;
   while (C % T) T >>= 1;
-  while (T > 256 && tree_stage_bytes(T, esz, pair) > (36u << 10)) T >>= 1;
+  while (T > 256 && 3 * tree_stage_max(T, esz, pair) > (uint32_t)kTreeSmem) T >>= 1;
   return T;
 }
 
@@ -770,14 +772,14 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
     const void* fn = HFR_BY_DTYPE(dt, HFR_TREE_TMA_FN);
     const uint32_t esz = (uint32_t)dtype_size(dt);
     const uint32_t T = tree_tile(C, esz, pair);
-    const int smem = kTreeStages * (int)tree_stage_bytes(T, esz, pair);
+    const int smem = kTreeSmem;
     HFR_TRY(allow_dynamic_smem(fn, smem));
     int occ = 0;
     HFR_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTreeThreads, smem));
     if (occ < 1) return HFR_ERR_UNSUPPORTED;
     const int per_sm = std::min(occ, 2);
     a.tree_tile = T;
-    a.tree_stages = kTreeStages;
+    a.tree_smem = smem;
     a.tree_sync = c->cfg.tree_sync;
     const uint64_t nt = (a.half_len[0] + T - 1) / T;  // tiles of the longer half
     for (uint64_t lo = 0; lo < std::max<uint64_t>(nt, 1); lo += kMaxChunks) {
@@ -789,7 +791,7 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
       g = std::max(2, std::min(g, kMaxCtas) & ~1);  // even: CTA b works on tree b & 1 only
       a.c_lo = (uint32_t)lo;
       a.c_hi = (uint32_t)hi;
-      a.sig = fnv(fnv(fnv(sig, (uint64_t)g * 1315423911ull + kTreeThreads), lo), 0x7474ull + T * 16 + kTreeStages);
+      a.sig = fnv(fnv(fnv(sig, (uint64_t)g * 1315423911ull + kTreeThreads), lo), 0x7474ull + T * 16);
       ++c->epoch;
       void* params[] = {&a};
       const cudaError_t e = launch_protocol_kernel(c, fn, dim3(g, c->local), dim3(kTreeThreads), params, smem, s, false);

@@ -36,7 +36,7 @@
 
 namespace hfr {
 
-constexpr int kTreeStagesMax = 4;
+constexpr int kTreeStagesMax = 8;
 constexpr int kTreeThreads = 128;  // 1 producer warp + 3 fold warps
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
@@ -52,8 +52,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_1() { asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// at most n (< kTreeStagesMax) most recent bulk groups still pending (n must be an immediate)
+__device__ __forceinline__ void bulk_wait_n(uint32_t n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.bulk.wait_group 5;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group 6;" ::: "memory"); break;
+  }
+}
 // generic-proxy accesses (an acquired flag, plain stores) vs async-proxy ones (bulk copies)
 __device__ __forceinline__ void fence_proxy_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -66,16 +77,27 @@ __device__ __forceinline__ bool mbar_wait_abort(uint64_t* bar, uint32_t parity, 
   }
 }
 
-// Stage geometry (bytes); the host computes the same (tree_stage_bytes).
+// Stage geometry (bytes) of one CTA's role: the regions its jobs use, each
+// rounded to 128 B.  The host sizes the tile so the largest role fits a third
+// of the shared-memory budget (tree_tile); a CTA then gets as many stages as
+// its own role fits (a DBT leaf, which only copies x, gets 8).
 struct TreeStage {
   uint32_t X, P, C0, C1, O, bytes;
-  __device__ __forceinline__ TreeStage(uint32_t T, uint32_t esz, bool pair) {
-    X = 0;
-    P = T * esz;
-    C0 = (pair ? 2u : 1u) * T * esz;
-    C1 = C0 + 4 * T;
-    O = C1 + 4 * T;
-    bytes = O + 4 * T;
+  __device__ __forceinline__ TreeStage(uint32_t T, uint32_t esz, bool pair, int nchild, const bool* raw,
+                                       bool compute, bool root) {
+    auto r128 = [](uint32_t v) { return (v + 127u) & ~127u; };
+    uint32_t off = 0;
+    X = off;
+    off += r128(T * esz);
+    P = off;
+    if (pair && compute) off += r128(T * esz);
+    C0 = off;
+    if (nchild > 0) off += r128(raw[0] ? T * esz : 4 * T);
+    C1 = off;
+    if (nchild > 1) off += r128(raw[1] ? T * esz : 4 * T);
+    O = off;
+    if (compute) off += r128(root ? T * esz : 4 * T);
+    bytes = off;
   }
 };
 
@@ -105,8 +127,6 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
   constexpr uint32_t esz = sizeof(typename E::T);
   constexpr uint32_t V = E::kPerVec;  // elements per 16 B: bulk copies move multiples of V
   const uint32_t T = a.tree_tile;
-  const uint32_t S = (uint32_t)a.tree_stages;
-  const TreeStage G(T, esz, PAIR);
   const int h = PAIR ? (rank & 1) : 0;
   const int me = PAIR ? (rank >> 1) : rank;
   const int partner = rank ^ 1;
@@ -124,6 +144,12 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
       for (int sl = 0; sl < nchild; ++sl) slot_raw[sl] = a.tree[p][nd.child[sl]].nchild == 0;
   }
   const bool has_down = !root && (nchild > 0 || PAIR);
+  const TreeStage G(T, esz, PAIR, nchild, slot_raw, !leafcopy, root);
+  // stages: as many as the role fits into the budget; D bulk-store groups in
+  // flight (one stage is being filled, one folded)
+  uint32_t S = (uint32_t)a.tree_smem / G.bytes;
+  S = S < (uint32_t)kTreeStagesMax ? S : (uint32_t)kTreeStagesMax;
+  const uint32_t D = S > 2 ? S - 2 : 1;
   const uint64_t base = a.half_base[h], len = a.half_len[h];
   const uint64_t R = (uint64_t)a.chunk / T;  // tiles per chunk
   Pad* const mypad = a.pad[rank];
@@ -182,6 +208,7 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
     // ------------------------------------------------------------ producer
     Tracer tr(a);
     uint64_t tq[kTreeStagesMax][3];  // trace: {t_first_poll, t_loaded, t_stored} per stage
+    bool plain[kTreeStagesMax];      // the stage's job also wrote with plain stores (ragged end)
     uint64_t loaded = 0, stored = 0, retired = 0;
     uint64_t t_poll = 0;           // first unsuccessful dependency poll of job `loaded`
     uint64_t t_idle = globaltimer();
@@ -284,6 +311,7 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
             bulk_s2g(slot + 4 * J.e0, sb + G.O, J.Lv * 4);
         }
       }
+      plain[st] = J.L > J.Lv;
       remainder(J);
     };
     auto raise = [&](const Job& J) {
@@ -296,9 +324,16 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
       }
     };
     // retire jobs [retired, upto): their bulk groups are complete
+    // Retire jobs [retired, upto): their bulk groups have COMPLETED (the
+    // writes are performed at the destination), so the flag store that follows
+    // cannot overtake them.  A system fence is needed only to order the plain
+    // stores of a ragged end before the flag (round-2 trace: a fence.acq_rel.sys
+    // per tile cost ~7 us and cut the TMA tree to 190 GB/s at n=2).
     auto retire_to = [&](uint64_t upto, uint64_t t_waited) {
+      bool fence = (a.tree_sync & 4) != 0;
+      for (uint64_t j = retired; j < upto; ++j) fence |= plain[j % S];
       if (!(a.tree_sync & 2)) fence_proxy_global();
-      if (!(a.tree_sync & 4)) fence_acq_rel_sys();  // ... and the remainder's plain stores
+      if (fence) fence_acq_rel_sys();
       const uint64_t t_fenced = tr.p ? globaltimer() : 0;
       for (; retired < upto; ++retired) {
         const Job J = job(retired);
@@ -345,9 +380,9 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
           if (tr.p) tq[st][2] = globaltimer();
           ++stored;
           did = true;
-          if (stored - retired > 1) {  // keep the newest group in flight, retire the older ones
-            bulk_wait_1();
-            retire_to(stored - 1, tr.p ? globaltimer() : 0);
+          if (stored - retired > D) {  // keep the newest D groups in flight, retire the older ones
+            bulk_wait_n(D);
+            retire_to(stored - D, tr.p ? globaltimer() : 0);
           }
         }
         stalled = false;  // a loaded job will become ready without any peer

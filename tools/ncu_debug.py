@@ -24,7 +24,7 @@ say("set_device")
 torch.zeros(1, device="cuda").sum().item()
 say("cuda context")
 dist.init_process_group("gloo")
-say("gloo up")
+say(f"gloo up: rank {dist.get_rank()} of {dist.get_world_size()}")
 comm = hfr.Comm.init(device=local, config=hfr.Config(algo="flat", timeout_ms=120000))
 say("comm init")
 t = comm.empty(1 << 20, torch.float32)
