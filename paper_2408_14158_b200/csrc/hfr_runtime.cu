@@ -267,7 +267,7 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
   if (c.flat_staging < 0 || c.flat_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   if (c.pdl_off != 0 && c.pdl_off != 1) return HFR_ERR_INVALID_ARGUMENT;
   if (c.tree_staging < 0 || c.tree_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
-  if (c.tree_sync < 0 || c.tree_sync > 7) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.tree_sync < 0 || c.tree_sync > 127) return HFR_ERR_INVALID_ARGUMENT;
   return HFR_SUCCESS;
 }
 
@@ -730,10 +730,10 @@ const void* tree_tma_fn(bool pair) {
 // third of the budget, so every role gets >= 3 stages.
 constexpr int kTreeSmem = 100 << 10;
 uint32_t tree_stage_max(uint32_t T, uint32_t esz, bool pair) { return T * esz * (pair ? 2 : 1) + 12 * T; }
-uint32_t tree_tile(uint64_t C, uint32_t esz, bool pair) {
-  uint32_t T = 2048;
+uint32_t tree_tile(uint64_t C, uint32_t esz, bool pair, uint32_t tmax = 2048, int budget = kTreeSmem) {
+  uint32_t T = tmax;
   while (C % T) T >>= 1;
-  while (T > 256 && 3 * tree_stage_max(T, esz, pair) > (uint32_t)kTreeSmem) T >>= 1;
+  while (T > 256 && 3 * tree_stage_max(T, esz, pair) > (uint32_t)budget) T >>= 1;
   return T;
 }
 
@@ -771,13 +771,15 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
 #define HFR_TREE_TMA_FN(E) tree_tma_fn<E>(pair)
     const void* fn = HFR_BY_DTYPE(dt, HFR_TREE_TMA_FN);
     const uint32_t esz = (uint32_t)dtype_size(dt);
-    const uint32_t T = tree_tile(C, esz, pair);
-    const int smem = kTreeSmem;
+    // EXPERIMENT (tree_sync bits 3-6): budget 100K / 200K (8) / 64K (16); tile max 2048 / 4096 (32) / 8192 (64)
+    const int xs = c->cfg.tree_sync;
+    const int smem = (xs & 8) ? (200 << 10) : (xs & 16) ? (64 << 10) : kTreeSmem;
+    const uint32_t T = tree_tile(C, esz, pair, (xs & 32) ? 4096u : (xs & 64) ? 8192u : 2048u, smem);
     HFR_TRY(allow_dynamic_smem(fn, smem));
     int occ = 0;
     HFR_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTreeThreads, smem));
     if (occ < 1) return HFR_ERR_UNSUPPORTED;
-    const int per_sm = std::min(occ, 2);
+    const int per_sm = std::min(occ, 3);
     a.tree_tile = T;
     a.tree_smem = smem;
     a.tree_sync = c->cfg.tree_sync;

@@ -39,8 +39,10 @@ def analyze(d):
         t0, t1, ts, t2 = (ev[:, k].astype(np.int64) for k in (1, 2, 3, 4))
         base = t0.min()
         rep = {"span_us": (t2.max() - base) / 1e3, "events": int(len(ev))}
-        for p, name in PH.items():
-            m = ph == p
+        # CTA parity = the tree a CTA works on (TMA tree kernel): split by role
+        cta_of = np.repeat(np.arange(tr.shape[0]), tr.shape[1])[tr.reshape(-1, 8)[:, 0] != 0]
+        for p, name in [(p, f"{nm}_tree{par}") for p, nm in PH.items() for par in (0, 1)]:
+            m = (ph == p) & ((cta_of & 1) == int(name[-1]))
             if not m.any():
                 continue
             rep[name] = {"n": int(m.sum()), "wait_us_sum": float((t1[m] - t0[m]).sum() / 1e3),
