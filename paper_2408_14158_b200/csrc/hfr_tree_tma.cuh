@@ -78,7 +78,7 @@ __device__ __forceinline__ bool mbar_wait_abort(uint64_t* bar, uint32_t parity, 
 }
 
 // Stage geometry (bytes) of one CTA's role: the regions its jobs use, each
-// rounded to 128 B.  The host sizes the tile so the largest role fits a third
+// rounded to 128 B; O (the output) usually aliases an input.  The host sizes the tile so the largest role fits a third
 // of the shared-memory budget (tree_tile); a CTA then gets as many stages as
 // its own role fits (a DBT leaf, which only copies x, gets 8).
 struct TreeStage {
@@ -95,8 +95,23 @@ struct TreeStage {
     if (nchild > 0) off += r128(raw[0] ? T * esz : 4 * T);
     C1 = off;
     if (nchild > 1) off += r128(raw[1] ? T * esz : 4 * T);
+    // The output overwrites an input of the same element size in place (each
+    // fold thread reads a unit completely before writing it back): the root's
+    // final values over x, a partial over an fp32 child partial, or over fp32
+    // x; only a 16/8-bit non-root node with raw (or no) children needs its own.
     O = off;
-    if (compute) off += r128(root ? T * esz : 4 * T);
+    if (compute) {
+      if (root)
+        O = X;
+      else if (nchild > 0 && !raw[0])
+        O = C0;
+      else if (nchild > 1 && !raw[1])
+        O = C1;
+      else if (esz == 4)
+        O = X;
+      else
+        off += r128(4 * T);
+    }
     bytes = off;
   }
 };
