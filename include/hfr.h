@@ -148,11 +148,11 @@ typedef struct {
     int pdl_off;          /* 1: launch the latency-bound kernels (ONESHOT, LL ONESHOT, barrier) of a
                              real comm as ordinary launches; 0 (default): programmatic dependent
                              launches (see hfr_allreduce).  Never changes results. */
-    int tree_staging;     /* DBT / PAIR_DBT data movement: 0 auto (= 2), 1 registers (SM loads/stores,
-                             one flag and one system fence per chunk), 2 TMA (bulk copies in and out of
-                             shared memory, one flag per tile of <= 2048 elements, raised when the
-                             tile's bulk stores completed).  Bits are identical either way. */
-    int tree_sync;        /* EXPERIMENT (round 2, to be removed): TMA tree fence variant bits */
+    int tree_staging;     /* DBT / PAIR_DBT data movement: 0 auto (= 1, measured faster), 1 registers
+                             (SM loads/stores, one flag and one system fence per chunk), 2 TMA (bulk
+                             copies in and out of shared memory, one flag per tile of <= 4096 elements,
+                             raised when the tile's bulk stores completed).  Bits are identical
+                             either way.  Part of the call signature. */
 } hfr_config_t;
 
 /* Fill *cfg with the defaults above (algo AUTO, scale 1.0). */

@@ -56,8 +56,7 @@ class _Config(ctypes.Structure):
                 ("threads", ctypes.c_int), ("scale", ctypes.c_float), ("scratch_bytes", ctypes.c_size_t),
                 ("timeout_ms", ctypes.c_int), ("oneshot_max_bytes", ctypes.c_size_t), ("stream_gate", ctypes.c_int),
                 ("nvls_bytes", ctypes.c_size_t), ("flat_staging", ctypes.c_int), ("ll_push_max", ctypes.c_size_t),
-                ("pdl_off", ctypes.c_int), ("tree_staging", ctypes.c_int),
-                ("tree_sync", ctypes.c_int)]
+                ("pdl_off", ctypes.c_int), ("tree_staging", ctypes.c_int)]
 
 
 @dataclass
@@ -77,7 +76,6 @@ class Config:
     ll_push_max: int = 0
     pdl_off: int = 0
     tree_staging: int = 0
-    tree_sync: int = 0
 
     def _c(self) -> _Config:
         if self.algo not in ALGOS:
@@ -85,7 +83,7 @@ class Config:
         return _Config(ALGOS[self.algo], self.chunk_elems, self.max_ctas, self.threads, self.scale,
                        self.scratch_bytes, self.timeout_ms, self.oneshot_max_bytes, self.stream_gate,
                        self.nvls_bytes, self.flat_staging, self.ll_push_max, self.pdl_off,
-                       self.tree_staging, self.tree_sync)
+                       self.tree_staging)
 
 
 _LIB = None

@@ -90,7 +90,6 @@ struct Args {
   uint64_t* trace;         // [local rank][CTA][trace_cap][4] u64, see Tracer
   uint32_t tree_tile;      // TMA tree kernel: elements per tile (flag granularity), divides chunk
   int tree_smem;           // TMA tree kernel: dynamic shared memory per CTA (each role fits its own stages)
-  int tree_sync;           // TMA tree kernel, experiment: fence variant bits (0 = default)
   TreeNode tree[2][kMaxRanks];
 };
 

@@ -267,7 +267,6 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
   if (c.flat_staging < 0 || c.flat_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   if (c.pdl_off != 0 && c.pdl_off != 1) return HFR_ERR_INVALID_ARGUMENT;
   if (c.tree_staging < 0 || c.tree_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
-  if (c.tree_sync < 0 || c.tree_sync > 127) return HFR_ERR_INVALID_ARGUMENT;
   return HFR_SUCCESS;
 }
 
@@ -762,7 +761,10 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
     a.buf[q] = bufs[q];
     a.part[q] = reinterpret_cast<float*>(stage_base(c, q) + area);
   }
-  const bool tma = c->cfg.tree_staging != 1;
+  // auto = register staging: the TMA form (hfr_tree_tma.cuh) measured slower
+  // at every size, n and dtype in round 2 (n=4 fp32 C2: DBT 404 vs 443 GB/s,
+  // PAIR 503 vs 595; n=2: 563 vs 598, 581 vs 625; bf16 1 GiB n=4: 304 vs 390)
+  const bool tma = c->cfg.tree_staging == 2;
   if (tma) {
     // hfr_tree_tma.cuh: one producer thread + 3 fold warps per CTA, flags per
     // tile, 3-stage shared-memory ring.  All CTAs of every rank must be
@@ -771,10 +773,11 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
 #define HFR_TREE_TMA_FN(E) tree_tma_fn<E>(pair)
     const void* fn = HFR_BY_DTYPE(dt, HFR_TREE_TMA_FN);
     const uint32_t esz = (uint32_t)dtype_size(dt);
-    // EXPERIMENT (tree_sync bits 3-6): budget 100K / 200K (8) / 64K (16); tile max 2048 / 4096 (32) / 8192 (64)
-    const int xs = c->cfg.tree_sync;
-    const int smem = (xs & 8) ? (200 << 10) : (xs & 16) ? (64 << 10) : kTreeSmem;
-    const uint32_t T = tree_tile(C, esz, pair, (xs & 32) ? 4096u : (xs & 64) ? 8192u : 2048u, smem);
+    // r02 sweep (n=2, C2 fp32): a 100 KiB budget at 2 CTAs/SM beats 200 KiB at
+    // 1/SM (557 vs 391 GB/s) and 64 KiB at 3/SM (489); 4096-element tiles
+    // +1 % over 2048 (profiles/r02/tree_tma_*.jsonl)
+    const int smem = kTreeSmem;
+    const uint32_t T = tree_tile(C, esz, pair, 4096u, smem);
     HFR_TRY(allow_dynamic_smem(fn, smem));
     int occ = 0;
     HFR_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kTreeThreads, smem));
@@ -782,7 +785,6 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
     const int per_sm = std::min(occ, 3);
     a.tree_tile = T;
     a.tree_smem = smem;
-    a.tree_sync = c->cfg.tree_sync;
     const uint64_t nt = (a.half_len[0] + T - 1) / T;  // tiles of the longer half
     for (uint64_t lo = 0; lo < std::max<uint64_t>(nt, 1); lo += kMaxChunks) {
       const uint64_t hi = lo + kMaxChunks;

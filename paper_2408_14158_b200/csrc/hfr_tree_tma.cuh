@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
       }
       mbar_expect_tx(&full[st], tx);
       if (!J.Lv) return;
-      if (!(a.tree_sync & 1)) fence_proxy_global();  // the acquired flags before the bulk reads
+      fence_proxy_global();  // the acquired flags before the bulk reads
       bulk_g2s(sb + G.X, a.buf[rank] + xb, xbytes, &full[st]);
       if (J.down) return;
       if (PAIR) bulk_g2s(sb + G.P, a.buf[partner] + xb, xbytes, &full[st]);
@@ -345,9 +345,9 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
     // stores of a ragged end before the flag (round-2 trace: a fence.acq_rel.sys
     // per tile cost ~7 us and cut the TMA tree to 190 GB/s at n=2).
     auto retire_to = [&](uint64_t upto, uint64_t t_waited) {
-      bool fence = (a.tree_sync & 4) != 0;
+      bool fence = false;
       for (uint64_t j = retired; j < upto; ++j) fence |= plain[j % S];
-      if (!(a.tree_sync & 2)) fence_proxy_global();
+      fence_proxy_global();
       if (fence) fence_acq_rel_sys();
       const uint64_t t_fenced = tr.p ? globaltimer() : 0;
       for (; retired < upto; ++retired) {

@@ -79,7 +79,6 @@ def main():
     ap.add_argument("--bytes", type=int, default=186 << 20)
     ap.add_argument("--out", default="gpurun_out/trace")
     ap.add_argument("--staging", type=int, default=0, help="hfr_config.tree_staging")
-    ap.add_argument("--sync", type=int, default=0, help="hfr_config.tree_sync (experiment)")
     a = ap.parse_args()
     if a.analyze:
         print(json.dumps(analyze(a.analyze), indent=1))
@@ -96,7 +95,7 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     comm = hfr.Comm.init(device=local, config=hfr.Config(algo=a.algo, chunk_elems=a.chunk, max_ctas=a.ctas,
                                                         scale=1.0 / dist.get_world_size(),
-                                                        tree_staging=a.staging, tree_sync=a.sync))
+                                                        tree_staging=a.staging))
     t = comm.empty(a.bytes // 4, torch.float32)
     t.normal_()
     for _ in range(3):
@@ -119,7 +118,7 @@ def main():
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     if rank == 0:
         n = dist.get_world_size()
-        print(json.dumps({"algo": a.algo, "chunk": a.chunk, "ctas": a.ctas, "staging": a.staging, "sync": a.sync,
+        print(json.dumps({"algo": a.algo, "chunk": a.chunk, "ctas": a.ctas, "staging": a.staging,
                           "n": n, "ms": float(ms),
                           "busbw": a.bytes / (float(ms) / 1e3) * 2 * (n - 1) / n / 1e9}))
     comm.finalize()
