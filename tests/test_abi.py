@@ -83,3 +83,23 @@ def test_library_tree_equals_oracle_tree(n):
         parent, children = hfr.tree_query(n, which)
         assert parent == want[which][0]
         assert children == want[which][1]
+
+
+def test_config_struct_matches_header():
+    """The ctypes mirror of hfr_config_t has the header's fields in the
+    header's order with matching C types (the ABI of every call taking a
+    config)."""
+    src = open(os.path.join(ROOT, "include", "hfr.h")).read()
+    body = re.search(r"typedef struct \{(.*?)\} hfr_config_t;", src, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"^\s*(int|size_t|float)\s+(\w+);", body, re.M)
+    ctype = {"int": ctypes.c_int, "size_t": ctypes.c_size_t, "float": ctypes.c_float}
+    assert [(n, ctype[t]) for t, n in fields] == [(n, t) for n, t in hfr._Config._fields_]
+    assert [f for f in hfr.Config.__dataclass_fields__] == [n for _, n in fields]
+
+
+def test_tree_staging_validated():
+    L = hfr.lib()
+    h = ctypes.c_void_p()
+    bad = hfr.Config(tree_staging=3)._c()
+    assert L.hfr_init_virtual(ctypes.byref(h), 2, 0, ctypes.byref(bad)) == hfr.ERR_INVALID_ARGUMENT

@@ -174,7 +174,10 @@ def main():
             tn = timeit(nfn, iters)
             emit({"impl": "nccl", "coll": a.coll, "n": n, "graph": a.graph, "dtype": a.dtype, "bytes": size,
                   "us": tn * 1e6, "busbw": size / tn * fac / 1e9, "algbw": size / tn / 1e9, **skew,
-                  "env": {k: v for k, v in os.environ.items() if k.startswith("NCCL_")}})
+                  # the loaded library's version (the image's NCCL_VERSION env names the system
+                  # libnccl, which torch does not load: VERDICT r01 weak #12)
+                  "nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                  "env": {k: v for k, v in os.environ.items() if k.startswith("NCCL_") and k != "NCCL_VERSION"}})
             del t_
     comm.finalize()
     if multi:
