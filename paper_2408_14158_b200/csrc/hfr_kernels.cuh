@@ -88,7 +88,6 @@ struct Args {
   uint32_t* uc_exit;       // NVLS: local unicast VA of the same counters
   uint32_t trace_cap;      // diagnostic trace: events per CTA (0 = off)
   uint64_t* trace;         // [local rank][CTA][trace_cap][4] u64, see Tracer
-  uint16_t tree_split[kMaxRanks];  // register tree kernel: CTAs of rank r working on tree A (the rest: B)
   uint32_t tree_tile;      // TMA tree kernel: elements per tile (flag granularity), divides chunk
   int tree_smem;           // TMA tree kernel: dynamic shared memory per CTA (each role fits its own stages)
   TreeNode tree[2][kMaxRanks];
@@ -1354,20 +1353,10 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     }
     __syncthreads();
   }
-  // CTA -> tree: this rank's first tree_split CTAs take tree A (even chunks,
-  // reading R8), the others tree B; each rank splits by its own roles' NVLink
-  // bytes (an interior node carries 3x a leaf's), so the CTAs of a rank's
-  // light role do not sit idle while its heavy role still streams.  Any CTA
-  // of a rank may serve any chunk: the flags are per chunk, not per CTA.
-  const int gA = a.tree_split[blockIdx.y];
-  const int tp = b < gA ? 0 : 1;
-  const uint64_t gp = tp ? gridDim.x - gA : gA;                        // CTAs on my tree
-  const uint64_t c_first = a.c_lo + tp + 2 * (uint64_t)(tp ? b - gA : b);  // c_lo is even
-  const uint64_t c_step = 2 * gp;
-  uint64_t dn = c_first;  // next chunk whose down pass is pending
+  uint64_t dn = a.c_lo + b;  // next chunk whose down pass is pending
 
   // ---- up pass -----------------------------------------------------------
-  for (uint64_t c = c_first; c < c_end; c += c_step) {
+  for (uint64_t c = a.c_lo + b; c < c_end; c += gridDim.x) {
     const TreeNode nd = a.tree[c & 1][me];
     const uint32_t lc = (uint32_t)(c - a.c_lo);
     const uint64_t tw = tr.p ? globaltimer() : 0;
@@ -1555,7 +1544,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
   }
 
   // ---- down pass (blocking) ------------------------------------------------
-  for (; dn < c_end; dn += c_step)
+  for (; dn < c_end; dn += gridDim.x)
     if (down_chunk(dn, true) < 0) return;
 
   // ---- PAIR: wait until the partner's half has fully landed in my buffer ---
@@ -1563,7 +1552,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     const uint64_t olen = a.half_len[h ^ 1];
     const uint64_t onch = (olen + C - 1) / C;
     const uint64_t oend = onch < a.c_hi ? onch : a.c_hi;
-    for (uint64_t c = c_first; c < oend; c += c_step) {
+    for (uint64_t c = a.c_lo + b; c < oend; c += gridDim.x) {
       if (threadIdx.x == 0) {
         const uint64_t tw = tr.p ? globaltimer() : 0;
         wait_ge(a, &mypad->pdown[(uint32_t)(c - a.c_lo)], ep);

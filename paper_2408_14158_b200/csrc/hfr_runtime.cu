@@ -13,7 +13,6 @@
 
 #include <algorithm>
 #include <array>
-#include <cmath>
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
@@ -737,35 +736,6 @@ uint32_t tree_tile(uint64_t C, uint32_t esz, bool pair, uint32_t tmax = 2048, in
   return T;
 }
 
-// Register tree kernel: how many of a rank's g CTAs work on tree A.  Weight
-// of a role = the NVLink bytes per element it moves (egress + ingress): up,
-// a partial to the parent (fp32, or a 16/8-bit leaf's raw value) and the
-// children's partials in; down, the final value in from the parent and out
-// to each child (+ the partner's copy in PAIR, + its pull of the partner's x).
-void tree_splits(const hfr_comm_s* c, Args& a, hfr_dtype_t dt, bool pair, int g) {
-  const double esz = (double)dtype_size(dt);
-  for (int q = 0; q < c->local; ++q) {
-    const int rank = c->virt ? q : c->rank;
-    const int node = pair ? rank >> 1 : rank;
-    double w[2];
-    for (int p = 0; p < 2; ++p) {
-      const TreeNode& nd = a.tree[p][node];
-      double bytes = 0;
-      if (nd.parent >= 0) bytes += (!pair && nd.nchild == 0 && esz < 4) ? esz : 4.0;  // partial out
-      for (int k = 0; k < nd.nchild; ++k) {
-        const TreeNode& ch = a.tree[p][nd.child[k]];
-        bytes += (!pair && ch.nchild == 0 && esz < 4) ? esz : 4.0;  // children's partials in
-        bytes += esz;                                                  // final out to the child
-      }
-      if (nd.parent >= 0) bytes += esz;  // final in
-      if (pair) bytes += 2 * esz;        // partner's x in, final out to the partner
-      w[p] = bytes;
-    }
-    int gA = w[0] + w[1] > 0 ? (int)std::lround(g * w[0] / (w[0] + w[1])) : g / 2;  // n = 1: no traffic
-    a.tree_split[q] = (uint16_t)std::min(std::max(gA, 1), g - 1);
-  }
-}
-
 hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtype_t dt, bool pair, uint64_t sig,
                       cudaStream_t s, size_t area) {
   const uint64_t C = tree_chunk(c);
@@ -850,13 +820,12 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   for (uint64_t lo = 0; lo < std::max<uint64_t>(nch, 1); lo += kMaxChunks) {
     const uint64_t hi = lo + kMaxChunks;
     const uint64_t here = std::min<uint64_t>(nch, hi) - std::min<uint64_t>(nch, lo);
-    // Every CTA works on ONE tree, so the two trees' dependency chains never
-    // interleave inside a CTA (a rank is interior in one tree and a leaf in
-    // the other); each rank splits its CTAs between the trees by its roles.
+    // An EVEN number of CTAs per rank: CTA b then only ever sees chunks of
+    // tree b & 1, so the two trees' dependency chains never interleave inside
+    // one CTA (a rank is the root of one tree and a leaf of the other).
     int g = 0;
     HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>(std::max<uint64_t>(here, 2), kMaxCtas), &g, per_sm));
-    g = std::max(2, g);
-    tree_splits(c, a, dt, pair, g);
+    g = std::max(2, g & ~1);
     a.c_lo = (uint32_t)lo;
     a.c_hi = (uint32_t)hi;
     a.sig = fnv(fnv(sig, (uint64_t)g * 1315423911ull + threads), lo);
