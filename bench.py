@@ -287,7 +287,8 @@ def nvlink_peak(probe):
     push or mixed pull/push — FLAT's own traffic is the mixed one)."""
     if not probe:
         return NVLINK_GUIDE_GBS, "fallback: B200_PROFILING.md peer copy 770 GB/s/dir (probe unavailable)"
-    keys = [k for k in probe if k.startswith(("read  (pull", "write (push", "mixed"))]
+    # every all-GPUs-at-once pattern, SM-driven or bulk-copy (TMA) driven
+    keys = [k for k in probe if k.startswith(("read  (pull", "write (push", "mixed", "tma push", "tma pull", "tma mixed"))]
     if not keys:
         return NVLINK_GUIDE_GBS, "fallback: B200_PROFILING.md peer copy 770 GB/s/dir (probe parse failed)"
     best = max(keys, key=lambda k: probe[k])
@@ -484,6 +485,7 @@ def main():
         achieved = nv_bytes / t_step / 1e9
         roof = {"bound": "nvlink", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "frac_of_nominal": achieved / NVLINK_NOMINAL_GBS,
+                "frac_of_guide": achieved / NVLINK_GUIDE_GBS,  # B200_PROFILING.md's measured peer copy
                 "nominal": NVLINK_NOMINAL_GBS,
                 "traffic": (max(trec.get("nvltx_bytes", 0), trec.get("nvlrx_bytes", 0)) or None) if trec else None,
                 "traffic_kind": "ncu nvltx/nvlrx bytes per launch, the larger direction (rank 0)",
