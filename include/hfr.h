@@ -140,8 +140,8 @@ typedef struct {
                              UNSUPPORTED.  0 (default): no arena. */
     int flat_staging;     /* FLAT kernel staging: 0 auto (TMA bulk copies into shared memory for n in
                              {2,4,8}, registers otherwise), 1 registers (no shared memory: small CTAs
-                             can share an SM with a compute kernel, e.g. DDP overlap), 2 TMA loads,
-                             3 TMA loads and TMA result stores.  Bits are identical either way. */
+                             can share an SM with a compute kernel, e.g. DDP overlap), 2 TMA.  Bits
+                             are identical either way. */
     size_t ll_push_max;   /* AUTO: largest (n-1) * count * 8 bytes a rank pushes in the LL ONESHOT
                              form before FLAT takes over; 0 -> 6 MiB (the r01 crossover on 2 and 4
                              B200s).  Part of the call signature (it picks the schedule). */

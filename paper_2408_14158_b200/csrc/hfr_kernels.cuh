@@ -80,7 +80,6 @@ struct Args {
   int src_rank;            // FLAT kernel: -1 fold all ranks; -2 copy my own shard; r>=0 copy rank r's
   uint32_t dst_mask;       // FLAT kernel: ranks that receive the result (0 = the owner itself)
   int tma_tile;            // FLAT TMA kernel: bytes per source per stage (multiple of 16)
-  int tma_store;           // FLAT TMA kernel: results leave through bulk copies (shared -> each rank)
   int excl_root;           // FLAT kernel: >= 0: this rank owns no shard (reduce/broadcast root)
   int nvls_op;             // NVLS kernel: bit0 multimem.ld_reduce (else local load), bit1 multimem.st (else local store)
   int nvls_solo;           // NVLS kernel: >= 0: this rank alone covers the whole buffer (reduce/broadcast root)
@@ -683,24 +682,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 constexpr int kTmaTileBytes = 4096;  // default bytes per source per stage (a.tma_tile)
 constexpr uint64_t kPairSubUnits = 256;  // PAIR tree kernel: 8-element units per partner sub-tile
 
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
                "r"(bytes)
                : "memory");
 }
 
-// Result stores: plain 16-B stores to every destination rank, or (a.tma_store)
-// the CTA writes the cast result tile into one of kOutStages shared-memory
-// out-stages and one thread bulk-copies it to every destination
-// (cp.async.bulk shared -> global, SASS UBLKCP), so NVLink pushes are issued
-// by the TMA engine too; an out-stage is reused once its bulk group has read
-// it (wait_group.read), and the kernel drains every group before the exit
-// handshake.
-constexpr int kOutStages = 4;
 template <class E, int NR>
 __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
-  extern __shared__ __align__(128) uint8_t stage_mem[];  // [2][NR][a.tma_tile] (+ [kOutStages][a.tma_tile])
+  extern __shared__ __align__(128) uint8_t stage_mem[];  // [2][NR][a.tma_tile]
   __shared__ uint64_t bars[2];
   __shared__ uint64_t s_tile[2];
   const int rank = a.rank0 + blockIdx.y;
@@ -710,7 +700,6 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
   // shard owners: all ranks, or (reduce) the n-1 ranks other than the root
   const int nown = a.excl_root >= 0 ? NR - 1 : NR;
   const int own = a.excl_root >= 0 ? (rank < a.excl_root ? rank : rank - 1) : rank;
-  const bool ts = a.tma_store != 0;
   if (entry_barrier(a, rank, b, e) && rank != a.excl_root) {
     constexpr int K = E::kPerVec;
     const uint64_t TB = (uint64_t)a.tma_tile;    // bytes per source per stage
@@ -718,7 +707,6 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
     const uint64_t nvec = a.count / K;
     const uint64_t lo = nvec * own / nown, hi = nvec * (own + 1) / nown;
     const uint64_t ntile = (hi - lo + TV - 1) / TV;
-    uint8_t* const out_mem = stage_mem + (size_t)2 * NR * TB;
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(&a.pad[rank]->tile_next);
     auto issue = [&](int st, uint64_t t) {  // thread 0 only
       const uint64_t v0 = lo + t * TV;
@@ -748,7 +736,6 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
       const uint64_t v0 = lo + t * TV;
       const uint64_t nv = v0 + TV < hi ? TV : hi - v0;
       const uint8_t* sm = stage_mem + (size_t)st * NR * TB;
-      uint8_t* om = out_mem + (size_t)(k % kOutStages) * TB;
       for (uint64_t j = threadIdx.x; j < nv; j += blockDim.x) {
         float acc[K], tt[K];
         E::widen(*reinterpret_cast<const uint4*>(sm + j * 16), acc);
@@ -761,25 +748,12 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
 #pragma unroll
         for (int q = 0; q < K; ++q) acc[q] = __fmul_rn(acc[q], a.scale);
         const uint4 o = E::narrow(acc);
-        if (ts) {
-          *reinterpret_cast<uint4*>(om + j * 16) = o;
-        } else {
 #pragma unroll
-          for (int r = 0; r < NR; ++r)
-            if ((dmask >> r) & 1u) st128(a.buf[r] + (v0 + j) * 16, o);
-        }
+        for (int r = 0; r < NR; ++r)
+          if ((dmask >> r) & 1u) st128(a.buf[r] + (v0 + j) * 16, o);
       }
-      if (ts) fence_proxy_async_smem();  // my out-stage writes before the bulk store reads them
-      __syncthreads();  // every thread is done reading stage st (and writing the out-stage)
+      __syncthreads();  // every thread is done reading stage st
       if (threadIdx.x == 0) {
-        if (ts) {
-#pragma unroll
-          for (int r = 0; r < NR; ++r)
-            if ((dmask >> r) & 1u) bulk_s2g(a.buf[r] + v0 * 16, om, (uint32_t)(nv * 16));
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          // the out-stage written next round (k+1) was last read by group k+1-kOutStages
-          asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kOutStages - 1) : "memory");
-        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem accesses before async proxy
         const uint64_t tn = atomicAdd(ctr, 1ull);
         s_tile[st] = tn;
@@ -787,7 +761,6 @@ __global__ void __launch_bounds__(256) hfr_flat_tma_kernel(const Args a) {
       }
       __syncthreads();
     }
-    if (ts && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // results landed
     // ragged tail (< K elements) — last owner, CTA 0
     const uint64_t t0 = nvec * K;
     if (own == nown - 1 && b == 0 && threadIdx.x < a.count - t0) {

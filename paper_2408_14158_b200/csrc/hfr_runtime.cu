@@ -264,7 +264,7 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
   if (!(c.scale == c.scale)) return HFR_ERR_INVALID_ARGUMENT;
   if (c.timeout_ms < 0) return HFR_ERR_INVALID_ARGUMENT;
   if (c.stream_gate != 0 && c.stream_gate != 1) return HFR_ERR_INVALID_ARGUMENT;
-  if (c.flat_staging < 0 || c.flat_staging > 3) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.flat_staging < 0 || c.flat_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   if (c.pdl_off != 0 && c.pdl_off != 1) return HFR_ERR_INVALID_ARGUMENT;
   if (c.tree_staging < 0 || c.tree_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   return HFR_SUCCESS;
@@ -663,8 +663,7 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
   const int tile = kTmaTileBytes;
   const int per_sm = c->virt && c->local > 1 ? 2 : 1;
   const int threads = cta_threads(c, 256);
-  const bool ts = c->cfg.flat_staging == 3;  // results out through bulk copies too
-  const int smem = 2 * c->n * tile + (ts ? kOutStages * tile : 0);
+  const int smem = 2 * c->n * tile;
   HFR_TRY(allow_dynamic_smem(fn, smem));
   int g = c->cfg.max_ctas > 0 ? c->cfg.max_ctas : per_sm * c->num_sms;
   // no more CTAs than tiles: idle CTAs would only add handshakes
@@ -678,10 +677,9 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
   }
   g = std::max(1, std::min(g, kMaxCtas));
   Args a;
-  base_args(c, a, count, fnv(fnv(sig, 0x544d41 + (ts ? 1 : 0)), (uint64_t)g * 1315423911ull + threads));
+  base_args(c, a, count, fnv(fnv(sig, 0x544d41), (uint64_t)g * 1315423911ull + threads));
   for (int q = 0; q < c->n; ++q) a.buf[q] = bufs[q];
   a.tma_tile = tile;
-  a.tma_store = ts ? 1 : 0;
   coll_routing(c, coll, root, &a.src_rank, &a.dst_mask, &a.excl_root);
   ++c->epoch;
   void* params[] = {&a};

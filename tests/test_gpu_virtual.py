@@ -432,34 +432,14 @@ def test_tree_many_tiles_segments(hfr, algo):
     comm.free_all()
 
 
-@pytest.mark.parametrize("staging", [1, 2, 3])
+@pytest.mark.parametrize("staging", [1, 2])
 @pytest.mark.parametrize("n", [2, 3, 4, 8])
 @pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16, gen.E5M2])
 @pytest.mark.parametrize("N", [7, 4096 + 13, 1_000_003])
 def test_flat_staging_modes(hfr, staging, n, dtype, N):
-    """FLAT with register staging (1), TMA loads (2) and TMA loads + TMA
-    result stores (3): the rank-ascending fold's bits in every mode."""
+    """FLAT with register staging (1) and TMA-staged loads (2; n = 3 has no
+    TMA instantiation and falls back to registers): the rank-ascending
+    fold's bits either way."""
     xs = gen.rank_inputs(n, N, dtype, "normal", seed_base=4400 + N)
     outs = run_cfg(hfr, n, xs, hfr.Config(algo="flat", scale=0.5, flat_staging=staging))
     check(outs, O.fold_ascending(xs, 0.5), f"flat staging={staging} n={n} {dtype} N={N}")
-
-
-@pytest.mark.parametrize("kind", ["reduce_scatter", "reduce", "allreduce"])
-@pytest.mark.parametrize("n", [2, 4, 8])
-def test_flat_tma_store_collectives(hfr, kind, n):
-    """TMA result stores honour the destination mask (reduce-scatter: the
-    owner only; reduce: the root only, which owns no shard)."""
-    comm = comm_for(hfr, n)
-    comm.set_config(hfr.Config(scale=0.5, flat_staging=3))
-    N = 300_007
-    xs = gen.rank_inputs(n, N, gen.BF16, "normal", seed_base=4500 + n)
-    bufs = comm.empty(N, torch.bfloat16)
-    for b, x in zip(bufs, xs):
-        b.copy_(to_torch(x, "cuda:0"))
-    comm.collective_virtual(kind, bufs, root=1)
-    torch.cuda.synchronize()
-    assert comm.status() == hfr.SUCCESS
-    want = {"reduce_scatter": lambda: O.reduce_scatter(xs, 0.5), "reduce": lambda: O.reduce(xs, 1, 0.5),
-            "allreduce": lambda: O.allreduce(xs, "flat", scale=0.5)}[kind]()
-    for r, b in enumerate(bufs):
-        assert_bit_exact(to_numpy(b), want[r], f"{kind} tma-store n={n} rank {r}")

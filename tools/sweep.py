@@ -32,7 +32,7 @@ def main():
     p.add_argument("--ctas", default="0")
     p.add_argument("--threads", default="0")
     p.add_argument("--tree-staging", default="0", help="comma list of hfr_config.tree_staging (0 auto, 1 regs, 2 TMA)")
-    p.add_argument("--flat-staging", default="0", help="comma list of hfr_config.flat_staging (0 auto, 1 regs, 2 TMA, 3 TMA in+out)")
+    p.add_argument("--flat-staging", default="0", help="comma list of hfr_config.flat_staging (0 auto, 1 regs, 2 TMA)")
     p.add_argument("--iters", type=int, default=0)
     p.add_argument("--nccl", action="store_true")
     p.add_argument("--graph", action="store_true", help="time `iters` calls captured in one CUDA graph")
