@@ -88,7 +88,6 @@ struct Args {
   uint32_t* uc_exit;       // NVLS: local unicast VA of the same counters
   uint32_t trace_cap;      // diagnostic trace: events per CTA (0 = off)
   uint64_t* trace;         // [local rank][CTA][trace_cap][4] u64, see Tracer
-  int tree_down_split;     // register tree kernel: separate CTAs for the up and the down pass
   uint32_t tree_tile;      // TMA tree kernel: elements per tile (flag granularity), divides chunk
   int tree_smem;           // TMA tree kernel: dynamic shared memory per CTA (each role fits its own stages)
   TreeNode tree[2][kMaxRanks];
@@ -1354,23 +1353,10 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     }
     __syncthreads();
   }
-  // CTA b works on tree b & 1 (gridDim.x and c_lo are even, so chunk c = c_lo
-  // + b + j * gridDim.x has parity b & 1).  With tree_down_split the tree's
-  // CTAs are split in two: the first half runs the up pass, the second the
-  // down pass, so an interior node forwards finished chunks to its children
-  // while its up pass is still streaming (round-2 trace, n=4: the down pass
-  // started only after a CTA's last up chunk, leaving the links of the
-  // interior ranks half used in each phase).
-  const uint64_t tp = (uint64_t)b & 1, idx = (uint64_t)b >> 1, per_tree = gridDim.x >> 1;
-  const bool split = a.tree_down_split && per_tree >= 2;
-  const uint64_t n_up = split ? (per_tree + 1) / 2 : per_tree, n_dn = split ? per_tree - n_up : per_tree;
-  const bool up_cta = !split || idx < n_up, down_cta = !split || idx >= n_up;
-  const uint64_t up_first = a.c_lo + tp + 2 * idx, up_step = 2 * n_up;
-  const uint64_t dn_step = 2 * n_dn;
-  uint64_t dn = a.c_lo + tp + 2 * (split ? idx - n_up : idx);  // next chunk whose down pass is pending
+  uint64_t dn = a.c_lo + b;  // next chunk whose down pass is pending
 
   // ---- up pass -----------------------------------------------------------
-  for (uint64_t c = up_first; up_cta && c < c_end; c += up_step) {
+  for (uint64_t c = a.c_lo + b; c < c_end; c += gridDim.x) {
     const TreeNode nd = a.tree[c & 1][me];
     const uint32_t lc = (uint32_t)(c - a.c_lo);
     const uint64_t tw = tr.p ? globaltimer() : 0;
@@ -1558,7 +1544,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
   }
 
   // ---- down pass (blocking) ------------------------------------------------
-  for (; down_cta && dn < c_end; dn += dn_step)
+  for (; dn < c_end; dn += gridDim.x)
     if (down_chunk(dn, true) < 0) return;
 
   // ---- PAIR: wait until the partner's half has fully landed in my buffer ---
@@ -1566,8 +1552,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     const uint64_t olen = a.half_len[h ^ 1];
     const uint64_t onch = (olen + C - 1) / C;
     const uint64_t oend = onch < a.c_hi ? onch : a.c_hi;
-    const uint64_t w_first = a.c_lo + tp + 2 * (split ? idx - n_up : idx);
-    for (uint64_t c = w_first; down_cta && c < oend; c += dn_step) {
+    for (uint64_t c = a.c_lo + b; c < oend; c += gridDim.x) {
       if (threadIdx.x == 0) {
         const uint64_t tw = tr.p ? globaltimer() : 0;
         wait_ge(a, &mypad->pdown[(uint32_t)(c - a.c_lo)], ep);

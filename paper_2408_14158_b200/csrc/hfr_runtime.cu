@@ -266,7 +266,7 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
   if (c.stream_gate != 0 && c.stream_gate != 1) return HFR_ERR_INVALID_ARGUMENT;
   if (c.flat_staging < 0 || c.flat_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   if (c.pdl_off != 0 && c.pdl_off != 1) return HFR_ERR_INVALID_ARGUMENT;
-  if (c.tree_staging < 0 || c.tree_staging > 3) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.tree_staging < 0 || c.tree_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   return HFR_SUCCESS;
 }
 
@@ -815,9 +815,7 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   // n=2 572 -> 591, but PAIR (shared-memory partner ring) 590-609 -> 561 and
   // bf16 DBT 388 -> 377, so those keep 2)
   const int threads = cta_threads(c, 256);
-  // EXPERIMENT (tree_staging 3): dedicated down-pass CTAs, twice the CTAs
-  a.tree_down_split = c->cfg.tree_staging == 3 ? 1 : 0;
-  const int per_sm = a.tree_down_split ? 8 : (!pair && dt == HFR_FLOAT32 ? 3 : 2);  // split: capped by occupancy
+  const int per_sm = !pair && dt == HFR_FLOAT32 ? 3 : 2;
   const uint64_t nch = (a.half_len[0] + C - 1) / C;  // half 0 is the longer one
   for (uint64_t lo = 0; lo < std::max<uint64_t>(nch, 1); lo += kMaxChunks) {
     const uint64_t hi = lo + kMaxChunks;
@@ -827,18 +825,10 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
     // one CTA (a rank is the root of one tree and a leaf of the other).
     int g = 0;
     HFR_TRY(ctas_per_rank(c, fn, threads, (int)std::min<uint64_t>(std::max<uint64_t>(here, 2), kMaxCtas), &g, per_sm));
-    if (a.tree_down_split) {
-      // a down-pass CTA waits on the root's UP-pass CTA of the same chunk (another
-      // index): every CTA must be resident, or a spinning CTA could hold the slot
-      // the awaited one needs
-      int occ = 0;
-      HFR_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0));
-      g = std::min(g, std::max(2, occ * c->num_sms / c->local));
-    }
     g = std::max(2, g & ~1);
     a.c_lo = (uint32_t)lo;
     a.c_hi = (uint32_t)hi;
-    a.sig = fnv(fnv(sig, (uint64_t)g * 1315423911ull + threads + a.tree_down_split), lo);
+    a.sig = fnv(fnv(sig, (uint64_t)g * 1315423911ull + threads), lo);
     HFR_TRY(launch(c, fn, g, threads, a, s));
   }
   return HFR_SUCCESS;
