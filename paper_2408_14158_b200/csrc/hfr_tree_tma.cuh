@@ -129,87 +129,6 @@ __device__ __forceinline__ void narrow8_generic(uint8_t* p, const float* f) {
   }
 }
 
-// Fold one stage (fold warps): for each of the Lv elements, the node value
-// x_v (fl32(x_2k + x_2k+1) in PAIR, lower rank first) combined in order with
-// the children's partials (R10: children below, x_v, children above); the root
-// scales once and casts; the output goes to G.O (in place over an input).
-template <class E, bool PAIR>
-__device__ __forceinline__ void tree_fold_stage(const uint8_t* sb, const TreeStage& G, uint32_t Lv, const TreeNode& nd,
-                                                int nchild, const bool* slot_raw, bool root, int h, float scale,
-                                                uint32_t ct, uint32_t nct) {
-  constexpr uint32_t esz = sizeof(typename E::T);
-  const uint8_t* X = sb + G.X;
-  const uint8_t* P = sb + G.P;
-  const uint8_t* C[2] = {sb + G.C0, sb + G.C1};
-  uint8_t* O = const_cast<uint8_t*>(sb) + G.O;
-  const uint32_t nu = Lv / 8;
-  for (uint32_t u = ct; u < nu; u += nct) {
-    float xv[8], pp[2][8], acc[8];
-    widen8_generic<E>(X + (size_t)u * 8 * esz, xv);
-    if constexpr (PAIR) {
-      float xp[8];
-      widen8_generic<E>(P + (size_t)u * 8 * esz, xp);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) xv[k] = h == 0 ? __fadd_rn(xv[k], xp[k]) : __fadd_rn(xp[k], xv[k]);
-    }
-#pragma unroll
-    for (int sl = 0; sl < 2; ++sl)
-      if (sl < nchild) {
-        if (slot_raw[sl]) {
-          widen8_generic<E>(C[sl] + (size_t)u * 8 * esz, pp[sl]);
-        } else {
-          const float4 lo = *reinterpret_cast<const float4*>(C[sl] + (size_t)u * 32);
-          const float4 hi = *reinterpret_cast<const float4*>(C[sl] + (size_t)u * 32 + 16);
-          pp[sl][0] = lo.x, pp[sl][1] = lo.y, pp[sl][2] = lo.z, pp[sl][3] = lo.w;
-          pp[sl][4] = hi.x, pp[sl][5] = hi.y, pp[sl][6] = hi.z, pp[sl][7] = hi.w;
-        }
-      }
-    // in-order combination: children below, x_v, children above (R10)
-    const int sp = nd.self_pos;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = sp == 0 ? xv[q] : pp[0][q];
-#pragma unroll
-    for (int k = 1; k <= 2; ++k) {
-      if (k > nchild) break;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float t = k == sp ? xv[q] : (k < sp ? pp[k][q] : pp[k - 1][q]);
-        acc[q] = __fadd_rn(acc[q], t);
-      }
-    }
-    if (root) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = __fmul_rn(acc[q], scale);
-      narrow8_generic<E>(O + (size_t)u * 8 * esz, acc);
-    } else {
-      *reinterpret_cast<float4*>(O + (size_t)u * 32) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      *reinterpret_cast<float4*>(O + (size_t)u * 32 + 16) = make_float4(acc[4], acc[5], acc[6], acc[7]);
-    }
-  }
-  // Lv % 8 elements (fp32 tiles can end on a 4-element boundary)
-  for (uint32_t i = nu * 8 + ct; i < Lv; i += nct) {
-    float xv = E::load1(reinterpret_cast<const char*>(X), i);
-    if constexpr (PAIR) {
-      const float xp = E::load1(reinterpret_cast<const char*>(P), i);
-      xv = h == 0 ? __fadd_rn(xv, xp) : __fadd_rn(xp, xv);
-    }
-    float acc = 0.f;
-    for (int k = 0; k <= nchild; ++k) {
-      float s = xv;
-      if (k != nd.self_pos) {
-        const int sl = k < nd.self_pos ? k : k - 1;
-        s = slot_raw[sl] ? E::load1(reinterpret_cast<const char*>(C[sl]), i)
-                         : reinterpret_cast<const float*>(C[sl])[i];
-      }
-      acc = k == 0 ? s : __fadd_rn(acc, s);
-    }
-    if (root)
-      E::store1(reinterpret_cast<char*>(O), i, __fmul_rn(acc, scale));
-    else
-      reinterpret_cast<float*>(O)[i] = acc;
-  }
-}
-
 template <class E, bool PAIR>
 __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -526,8 +445,77 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
       if (!mbar_wait_abort(&full[st], (uint32_t)((j / S) & 1), &s_abort)) break;
       const Job J = job(j);
       if (is_compute(J)) {
-        tree_fold_stage<E, PAIR>(smem + (size_t)st * G.bytes, G, J.Lv, nd, nchild, slot_raw, root, h, a.scale, ct,
-                                 nct);
+        const uint8_t* sb = smem + (size_t)st * G.bytes;
+        const uint8_t* X = sb + G.X;
+        const uint8_t* P = sb + G.P;
+        const uint8_t* C[2] = {sb + G.C0, sb + G.C1};
+        uint8_t* O = const_cast<uint8_t*>(sb) + G.O;
+        const uint32_t nu = J.Lv / 8;
+        for (uint32_t u = ct; u < nu; u += nct) {
+          float xv[8], pp[2][8], acc[8];
+          widen8_generic<E>(X + (size_t)u * 8 * esz, xv);
+          if constexpr (PAIR) {
+            float xp[8];
+            widen8_generic<E>(P + (size_t)u * 8 * esz, xp);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) xv[k] = h == 0 ? __fadd_rn(xv[k], xp[k]) : __fadd_rn(xp[k], xv[k]);
+          }
+#pragma unroll
+          for (int sl = 0; sl < 2; ++sl)
+            if (sl < nchild) {
+              if (slot_raw[sl]) {
+                widen8_generic<E>(C[sl] + (size_t)u * 8 * esz, pp[sl]);
+              } else {
+                const float4 lo = *reinterpret_cast<const float4*>(C[sl] + (size_t)u * 32);
+                const float4 hi = *reinterpret_cast<const float4*>(C[sl] + (size_t)u * 32 + 16);
+                pp[sl][0] = lo.x, pp[sl][1] = lo.y, pp[sl][2] = lo.z, pp[sl][3] = lo.w;
+                pp[sl][4] = hi.x, pp[sl][5] = hi.y, pp[sl][6] = hi.z, pp[sl][7] = hi.w;
+              }
+            }
+          // in-order combination: children below, x_v, children above (R10)
+          const int sp = nd.self_pos;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = sp == 0 ? xv[q] : pp[0][q];
+#pragma unroll
+          for (int k = 1; k <= 2; ++k) {
+            if (k > nchild) break;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float t = k == sp ? xv[q] : (k < sp ? pp[k][q] : pp[k - 1][q]);
+              acc[q] = __fadd_rn(acc[q], t);
+            }
+          }
+          if (root) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = __fmul_rn(acc[q], a.scale);
+            narrow8_generic<E>(O + (size_t)u * 8 * esz, acc);
+          } else {
+            *reinterpret_cast<float4*>(O + (size_t)u * 32) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            *reinterpret_cast<float4*>(O + (size_t)u * 32 + 16) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+          }
+        }
+        // Lv % 8 elements (fp32 tiles can end on a 4-element boundary)
+        for (uint32_t i = nu * 8 + ct; i < J.Lv; i += nct) {
+          float xv = E::load1(reinterpret_cast<const char*>(X), i);
+          if constexpr (PAIR) {
+            const float xp = E::load1(reinterpret_cast<const char*>(P), i);
+            xv = h == 0 ? __fadd_rn(xv, xp) : __fadd_rn(xp, xv);
+          }
+          float acc = 0.f;
+          for (int k = 0; k <= nchild; ++k) {
+            float s = xv;
+            if (k != nd.self_pos) {
+              const int sl = k < nd.self_pos ? k : k - 1;
+              s = slot_raw[sl] ? E::load1(reinterpret_cast<const char*>(C[sl]), i)
+                               : reinterpret_cast<const float*>(C[sl])[i];
+            }
+            acc = k == 0 ? s : __fadd_rn(acc, s);
+          }
+          if (root)
+            E::store1(reinterpret_cast<char*>(O), i, __fmul_rn(acc, a.scale));
+          else
+            reinterpret_cast<float*>(O)[i] = acc;
+        }
         fence_proxy_smem();  // my shared-memory writes before the producer's bulk store reads them
       }
       __syncwarp();
