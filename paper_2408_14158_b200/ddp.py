@@ -31,11 +31,16 @@ differs from the comm's raises instead of silently summing where the caller
 averages.  finish() restores the comm's config.
 
 Measured on 4 B200s with a 7e9-parameter LLaMA-shaped backward (C5, median
-of 15 interleaved repetitions): the best bit-exact setting is FLAT with
-derive(comm, max_ctas=32..40, threads=128, stream_gate=1, flat_staging=1) —
-small register-staged comm CTAs (no shared memory) share SMs with the GEMM
-CTAs — plus a full-width tail_config, for an overlap of 0.90-0.95 over runs;
-algo "nvls" (order-relaxed) with 16 CTAs reaches 0.98-0.99.
+of 15 interleaved repetitions, profiles/r02/c5_ddp_r02r_3x_n4.jsonl): the
+best bit-exact setting by the step time (backward + exposed allreduce) is
+FLAT with derive(comm, max_ctas=32, threads=256, stream_gate=1,
+flat_staging=1) — register-staged comm CTAs (no shared memory) that share
+SMs with the GEMM CTAs — plus a full-width tail_config: 1.05x the backward
+alone, 0.82 of the full-width allreduce time hidden (3 runs: 0.817, 0.819,
+0.821).  threads=128 throttles the comm further (overlap 0.87-0.88 against
+its own, longer allreduce time, 0.76-0.79 against the full-width one, and a
+1 ms longer step).  algo "nvls" (order-relaxed) with 16 CTAs: 0.85 of the
+full-width time, 1.045x.
 """
 from __future__ import annotations
 

@@ -51,15 +51,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tokens", type=int, default=4096)
     ap.add_argument("--bucket-mib", type=int, default=64)
-    ap.add_argument("--max-ctas", type=int, default=24)
+    ap.add_argument("--max-ctas", type=int, default=32)
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--algo", default="flat")
     ap.add_argument("--layers", type=int, default=LAYERS, help="fewer layers for a quick run")
-    ap.add_argument("--gate", type=int, default=0, help="hfr_config.stream_gate")
-    ap.add_argument("--threads", type=int, default=0, help="threads per comm CTA (small CTAs can share an SM "
+    ap.add_argument("--gate", type=int, default=1, help="hfr_config.stream_gate")
+    ap.add_argument("--threads", type=int, default=256, help="threads per comm CTA (small CTAs can share an SM "
                                                           "with a GEMM CTA)")
-    ap.add_argument("--staging", type=int, default=0, help="hfr_config.flat_staging (1 = registers)")
-    ap.add_argument("--tail", type=int, default=0, help="1: buckets completed by the last gradient GEMM (embed) "
+    ap.add_argument("--staging", type=int, default=1, help="hfr_config.flat_staging (1 = registers)")
+    ap.add_argument("--tail", type=int, default=1, help="1: buckets completed by the last gradient GEMM (embed) "
                                                        "use a full-width config (nothing left to overlap)")
     ap.add_argument("--tail-algo", default="flat")
     a = ap.parse_args()
