@@ -149,12 +149,10 @@ typedef struct {
                              real comm as ordinary launches; 0 (default): programmatic dependent
                              launches (see hfr_allreduce).  Never changes results. */
     int tree_staging;     /* DBT / PAIR_DBT data movement: 0 auto (= 1, measured faster), 1 registers
-                             (SM loads/stores, one flag and one system fence per chunk), 2 TMA push
-                             (bulk copies in and out of shared memory, one flag per tile of <= 4096
-                             elements, raised when the tile's remote bulk stores completed), 3 TMA
-                             pull (every NVLink transfer a bulk-copy read; all stores local; an exit
-                             handshake).  Bits are identical in every mode.  Part of the call
-                             signature. */
+                             (SM loads/stores, one flag and one system fence per chunk), 2 TMA (bulk
+                             copies in and out of shared memory, one flag per tile of <= 4096 elements,
+                             raised when the tile's bulk stores completed).  Bits are identical
+                             either way.  Part of the call signature. */
 } hfr_config_t;
 
 /* Fill *cfg with the defaults above (algo AUTO, scale 1.0). */

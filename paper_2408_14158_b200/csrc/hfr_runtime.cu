@@ -24,7 +24,6 @@
 
 #include "../../include/hfr.h"
 #include "hfr_kernels.cuh"
-#include "hfr_tree_pull.cuh"
 #include "hfr_tree_tma.cuh"
 
 using namespace hfr;
@@ -267,7 +266,7 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
   if (c.stream_gate != 0 && c.stream_gate != 1) return HFR_ERR_INVALID_ARGUMENT;
   if (c.flat_staging < 0 || c.flat_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   if (c.pdl_off != 0 && c.pdl_off != 1) return HFR_ERR_INVALID_ARGUMENT;
-  if (c.tree_staging < 0 || c.tree_staging > 3) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.tree_staging < 0 || c.tree_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   return HFR_SUCCESS;
 }
 
@@ -722,10 +721,6 @@ template <class E>
 const void* tree_tma_fn(bool pair) {
   return pair ? (const void*)hfr_tree_tma_kernel<E, true> : (const void*)hfr_tree_tma_kernel<E, false>;
 }
-template <class E>
-const void* tree_pull_fn(bool pair) {
-  return pair ? (const void*)hfr_tree_pull_kernel<E, true> : (const void*)hfr_tree_pull_kernel<E, false>;
-}
 
 // TMA tree kernel geometry (hfr_tree_tma.cuh TreeStage): a 100 KiB
 // shared-memory budget per CTA (2 CTAs per SM); the tile is the largest power
@@ -769,16 +764,14 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   // auto = register staging: the TMA form (hfr_tree_tma.cuh) measured slower
   // at every size, n and dtype in round 2 (n=4 fp32 C2: DBT 404 vs 443 GB/s,
   // PAIR 503 vs 595; n=2: 563 vs 598, 581 vs 625; bf16 1 GiB n=4: 304 vs 390)
-  const bool tma = c->cfg.tree_staging == 2 || c->cfg.tree_staging == 3;
-  const bool pull = c->cfg.tree_staging == 3;
+  const bool tma = c->cfg.tree_staging == 2;
   if (tma) {
     // hfr_tree_tma.cuh: one producer thread + 3 fold warps per CTA, flags per
     // tile, 3-stage shared-memory ring.  All CTAs of every rank must be
     // co-resident (a CTA spins on tiles of peers' CTAs), so the grid is capped
     // by the occupancy at this shared-memory size.
 #define HFR_TREE_TMA_FN(E) tree_tma_fn<E>(pair)
-#define HFR_TREE_PULL_FN(E) tree_pull_fn<E>(pair)
-    const void* fn = pull ? HFR_BY_DTYPE(dt, HFR_TREE_PULL_FN) : HFR_BY_DTYPE(dt, HFR_TREE_TMA_FN);
+    const void* fn = HFR_BY_DTYPE(dt, HFR_TREE_TMA_FN);
     const uint32_t esz = (uint32_t)dtype_size(dt);
     // r02 sweep (n=2, C2 fp32): a 100 KiB budget at 2 CTAs/SM beats 200 KiB at
     // 1/SM (557 vs 391 GB/s) and 64 KiB at 3/SM (489); 4096-element tiles
@@ -802,12 +795,12 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
       g = std::max(2, std::min(g, kMaxCtas) & ~1);  // even: CTA b works on tree b & 1 only
       a.c_lo = (uint32_t)lo;
       a.c_hi = (uint32_t)hi;
-      a.sig = fnv(fnv(fnv(sig, (uint64_t)g * 1315423911ull + kTreeThreads), lo), 0x7474ull + T * 16 + pull);
+      a.sig = fnv(fnv(fnv(sig, (uint64_t)g * 1315423911ull + kTreeThreads), lo), 0x7474ull + T * 16);
       ++c->epoch;
       void* params[] = {&a};
       const cudaError_t e = launch_protocol_kernel(c, fn, dim3(g, c->local), dim3(kTreeThreads), params, smem, s, false);
       if (e != cudaSuccess) {
-        note_cuda(e, pull ? "hfr_tree_pull_kernel" : "hfr_tree_tma_kernel");
+        note_cuda(e, "hfr_tree_tma_kernel");
         return HFR_ERR_CUDA;
       }
       ++c->launches;

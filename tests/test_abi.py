@@ -101,5 +101,5 @@ def test_config_struct_matches_header():
 def test_tree_staging_validated():
     L = hfr.lib()
     h = ctypes.c_void_p()
-    bad = hfr.Config(tree_staging=4)._c()
+    bad = hfr.Config(tree_staging=3)._c()
     assert L.hfr_init_virtual(ctypes.byref(h), 2, 0, ctypes.byref(bad)) == hfr.ERR_INVALID_ARGUMENT
