@@ -32,6 +32,7 @@ def main():
     p.add_argument("--ctas", default="0")
     p.add_argument("--threads", default="0")
     p.add_argument("--tree-staging", default="0", help="comma list of hfr_config.tree_staging (0 auto, 1 regs, 2 TMA)")
+    p.add_argument("--pdl", default="0", help="comma list of hfr_config.pdl_off values")
     p.add_argument("--flat-staging", default="0", help="comma list of hfr_config.flat_staging (0 auto, 1 regs, 2 TMA)")
     p.add_argument("--iters", type=int, default=0)
     p.add_argument("--nccl", action="store_true")
@@ -143,15 +144,16 @@ def main():
         cnt = size // esz
         views = [b[:cnt] for b in bufs]
         iters = a.iters or (200 if size <= (1 << 20) else 50 if size <= (64 << 20) else 20)
-        for algo, chunk, ctas, thr, tst, fst in itertools.product(a.algos.split(","), map(int, a.chunks.split(",")),
-                                                                  map(int, a.ctas.split(",")),
-                                                                  map(int, a.threads.split(",")),
-                                                                  map(int, a.tree_staging.split(",")),
-                                                                  map(int, a.flat_staging.split(","))):
+        for algo, chunk, ctas, thr, tst, fst, pdl in itertools.product(a.algos.split(","), map(int, a.chunks.split(",")),
+                                                                       map(int, a.ctas.split(",")),
+                                                                       map(int, a.threads.split(",")),
+                                                                       map(int, a.tree_staging.split(",")),
+                                                                       map(int, a.flat_staging.split(",")),
+                                                                       map(int, a.pdl.split(","))):
             if algo == "pair_dbt" and n % 2:
                 continue
             comm.set_config(hfr.Config(algo=algo if algo != "barrier" else "auto", chunk_elems=chunk, max_ctas=ctas, threads=thr,
-                                       scale=1.0 / n, timeout_ms=30000, tree_staging=tst, flat_staging=fst))
+                                       scale=1.0 / n, timeout_ms=30000, tree_staging=tst, flat_staging=fst, pdl_off=pdl))
             if algo == "barrier":   # handshake latency only (hfr_barrier kernel)
                 fn = lambda: comm.barrier(torch.cuda.current_stream())  # noqa: E731
             elif multi:
@@ -163,7 +165,7 @@ def main():
             if st != hfr.SUCCESS:
                 raise SystemExit(f"hfr error {hfr.status_string(st)}")
             emit({"impl": "hfr", "coll": a.coll, "n": n, "virtual": not multi, "graph": a.graph, "dtype": a.dtype,
-                  "bytes": size, "algo": algo, "chunk": chunk, "ctas": ctas, "threads": thr, "tree_staging": tst, "flat_staging": fst,
+                  "bytes": size, "algo": algo, "chunk": chunk, "ctas": ctas, "threads": thr, "tree_staging": tst, "flat_staging": fst, "pdl_off": pdl,
                   "us": t * 1e6,
                   "busbw": size / t * fac / 1e9, "algbw": size / t / 1e9, **skew})
         if multi and a.nccl:
