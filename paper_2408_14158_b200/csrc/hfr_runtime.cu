@@ -265,7 +265,7 @@ hfr_status_t validate_cfg(const hfr_config_t& c) {
   if (c.timeout_ms < 0) return HFR_ERR_INVALID_ARGUMENT;
   if (c.stream_gate != 0 && c.stream_gate != 1) return HFR_ERR_INVALID_ARGUMENT;
   if (c.flat_staging < 0 || c.flat_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
-  if (c.pdl_off < 0 || c.pdl_off > 2) return HFR_ERR_INVALID_ARGUMENT;
+  if (c.pdl_off != 0 && c.pdl_off != 1) return HFR_ERR_INVALID_ARGUMENT;
   if (c.tree_staging < 0 || c.tree_staging > 2) return HFR_ERR_INVALID_ARGUMENT;
   return HFR_SUCCESS;
 }
@@ -550,7 +550,7 @@ const void* tree_fn(bool pair) {
 cudaError_t launch_protocol_kernel(const hfr_comm_s* c, const void* fn, dim3 grid, dim3 block, void** params,
                                    size_t smem, cudaStream_t s, bool pdl_ok) {
   if (c->virt && c->local > 1) return cudaLaunchCooperativeKernel(fn, grid, block, params, smem, s);
-  if (!pdl_ok || c->cfg.pdl_off == 1) return cudaLaunchKernel(fn, grid, block, params, smem, s);
+  if (!pdl_ok || c->cfg.pdl_off) return cudaLaunchKernel(fn, grid, block, params, smem, s);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -683,8 +683,7 @@ hfr_status_t run_flat_tma(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_
   coll_routing(c, coll, root, &a.src_rank, &a.dst_mask, &a.excl_root);
   ++c->epoch;
   void* params[] = {&a};
-  // EXPERIMENT (pdl_off = 2): programmatic dependent launch for FLAT-TMA too
-  cudaError_t e = launch_protocol_kernel(c, fn, dim3(g, c->local), dim3(threads), params, smem, s, c->cfg.pdl_off == 2);
+  cudaError_t e = launch_protocol_kernel(c, fn, dim3(g, c->local), dim3(threads), params, smem, s, false);
   if (e != cudaSuccess) {
     note_cuda(e, "hfr_flat_tma_kernel");
     return HFR_ERR_CUDA;
