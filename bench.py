@@ -185,7 +185,20 @@ def cpu_baseline(n: int, count: int, dtype: str, esz: int, multi: bool, budget_s
     t1m = statistics.median(t1)
     def metric(b, t):
         return headline(b, t, n, multi)
+    # SURVEY §8(d) also asks for GB/s over the (n+1)*S bytes the fold touches
+    # and the Python oracle's time on C1 (2 ranks x 4096 fp32)
+    import hfr_inputs as gen
+    from oracle import hfr_oracle as O
+    c1 = gen.rank_inputs(2, 4096, gen.FP32, "normal", seed_base=1234)
+    O.fold_ascending(c1)
+    tp = []
+    for _ in range(20):
+        t0 = time.perf_counter()
+        O.fold_ascending(c1)
+        tp.append(time.perf_counter() - t0)
     return {"value": metric(S, tc), "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "touched_gbs": (n + 1) * S / tc / 1e9,
+            "c1_python_oracle_ms": statistics.median(tp) * 1e3,
             "sample": f"full workload ({n} x {count} {dtype}), oracle/fold.c rank-ascending fold, median of "
                       f"{len(times)} reps (~{budget_s:.0f} s), {'busBW' if multi else 'algBW'}-equivalent",
             "one_thread": {"value": metric(small * esz, t1m), "unit": "GB/s", "cores": 1,
