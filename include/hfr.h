@@ -220,7 +220,7 @@ hfr_status_t hfr_deregister(hfr_comm_t comm, void* ptr);
  *   their small-message kernels as programmatic dependent launches: a kernel
  *   may become resident while the previous kernel on the stream finishes, but
  *   touches no memory before that kernel has completed (griddepcontrol.wait),
- *   so the ordering above is unchanged (HFR_PDL=0: ordinary launches).
+ *   so the ordering above is unchanged (config pdl_off = 1: ordinary launches).
  *   Result: every rank's buf holds identical bytes: the rank-ascending fold
  *   (FLAT), the tree-order fold (DBT) or the pair-first fold (PAIR_DBT), times
  *   scale, cast to dtype.  Buffers outside hfr_mem_alloc / hfr_register memory

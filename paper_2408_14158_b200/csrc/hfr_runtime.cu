@@ -545,8 +545,9 @@ const void* tree_fn(bool pair) {
 // in hardware (pdl_wait, hfr_kernels.cuh) before touching memory.  r01, n=2,
 // bf16, CUDA graph: 1 KiB 3.93 -> 3.75 us, 64 KiB 5.12 -> 4.73, 1 MiB 12.38 ->
 // 11.98; the bandwidth kernels (FLAT, FLAT-TMA) measured slower with it at
-// 2-64 MiB eager (2 MiB 17.3 -> 20.5 us), so they launch plainly
-// (profiles/r01/pdl_ab_n2.jsonl).  hfr_config_t.pdl_off = 1: never.
+// 2-64 MiB eager (2 MiB 17.3 -> 20.5 us) and neutral (+-0.3 %) back to back
+// at 4 MiB-1 GiB (r02), so they launch plainly (profiles/r01/pdl_ab_n2.jsonl,
+// profiles/r02/flat_pdl_ab.jsonl).  hfr_config_t.pdl_off = 1: never.
 cudaError_t launch_protocol_kernel(const hfr_comm_s* c, const void* fn, dim3 grid, dim3 block, void** params,
                                    size_t smem, cudaStream_t s, bool pdl_ok) {
   if (c->virt && c->local > 1) return cudaLaunchCooperativeKernel(fn, grid, block, params, smem, s);

@@ -167,7 +167,7 @@ def main():
         print(json.dumps({
             "config": "C5 HaiScale DDP", "n": n, "params": ddp.total, "grad_bytes": S,
             "buckets": len(ddp.bucket_ranges), "bucket_mib": a.bucket_mib, "max_ctas": a.max_ctas, "algo": a.algo,
-            "stream_gate": a.gate, "threads": a.threads, "flat_staging": a.staging, "side_priority": os.environ.get("HFR_SIDE_PRIORITY", "high"),
+            "stream_gate": a.gate, "threads": a.threads, "flat_staging": a.staging,
             "tokens": T, "T_bwd_ms": tb * 1e3, "T_comm_ms": tc * 1e3, "T_both_ms": tt * 1e3,
             "overlap": (tb + tc - tt) / tc, "bwd_slowdown": tt / tb,
             "T_comm_full_ms": tf * 1e3,
