@@ -50,3 +50,31 @@ def test_hfr_arm_schema_tiny():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= 3
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= d["clocks"].keys()
+
+
+@pytest.mark.parametrize("algo,n,esz,want", [
+    # SURVEY §8(d) "algorithmic bytes": worst rank's NVLink bytes per direction, in units of S
+    ("dbt", 8, 4, 2.0), ("dbt", 4, 4, 2.0), ("dbt", 2, 4, 1.0),
+    ("pair_dbt", 8, 4, 2.0), ("pair_dbt", 4, 4, 1.5),
+    ("nvls", 8, 4, 1.125), ("nvls", 4, 2, 1.25), ("nvls", 2, 4, 1.5),
+])
+def test_variant_bytes_match_survey(algo, n, esz, want):
+    """bench.variant_dir_bytes (the roofline numerator of the tree/NVLS
+    variants) reproduces SURVEY §8(d)'s per-direction byte counts, computed
+    from the library's own trees (hfr_tree_query, host-only)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2408_14158_b200 as hfr
+    S = 1 << 20
+    assert bench.variant_dir_bytes(hfr, algo, n, S, esz) == pytest.approx(want * S)
+
+
+def test_variant_bytes_bf16_dbt_between_2_and_3():
+    """bf16 DBT: fp32 partials up (16-bit leaves send raw values), bf16 finals
+    down — SURVEY's 3S is the all-fp32-partials upper bound."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2408_14158_b200 as hfr
+    S = 1 << 20
+    v = bench.variant_dir_bytes(hfr, "dbt", 8, S, 2) / S
+    assert 2.0 <= v <= 3.0
