@@ -221,6 +221,9 @@ def reference_arm(args):
     import hfr_inputs as gen
     from oracle import cfold
     xs = gen.rank_inputs(n, count, dtype, "grad", seed_base=1000)
+    # all host cores: torchrun sets OMP_NUM_THREADS=1 for its workers, which
+    # would time the oracle on one core at N > 1
+    cfold.set_threads(os.cpu_count() or 1)
     for _ in range(args.warmup):
         cfold.fold_ascending(xs, 1.0 / n)
     t0 = time.perf_counter()
