@@ -632,11 +632,12 @@ def main():
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-            "config": dict(workload_config(args, n, count, dtype), clock_soak_s=args.soak),
+            # the same config object as the reference arm's (the driver compares them)
+            "config": workload_config(args, n, count, dtype),
             "value_definition": value_definition(multi),
             "algbw": algbw(S, t_step), "busbw_virtual": None if multi else busbw(S, t_step, n),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches, "clocks": ck, "nccl": nccl, "variants": variants,
+            "gpu_launches": launches, "clocks": dict(ck or {}, soak_s=args.soak), "nccl": nccl, "variants": variants,
         }
         print(json.dumps(line), flush=True)
     comm.finalize()
