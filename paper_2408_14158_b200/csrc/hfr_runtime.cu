@@ -768,7 +768,7 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   const bool tma = c->cfg.tree_staging == 2;
   if (tma) {
     // hfr_tree_tma.cuh: one producer thread + 3 fold warps per CTA, flags per
-    // tile, 3-stage shared-memory ring.  All CTAs of every rank must be
+    // tile, a shared-memory ring of 3-8 stages (by role).  All CTAs of every rank must be
     // co-resident (a CTA spins on tiles of peers' CTAs), so the grid is capped
     // by the occupancy at this shared-memory size.
 #define HFR_TREE_TMA_FN(E) tree_tma_fn<E>(pair)
@@ -814,7 +814,11 @@ hfr_status_t run_tree(hfr_comm_s* c, char* const* bufs, uint64_t count, hfr_dtyp
   // chunk's stores at the per-chunk system fence the others issue (r01, n=4:
   // DBT 1 -> 2 CTAs/SM 377 -> 422 GB/s; fp32 DBT 2 -> 3 CTAs/SM 423 -> 442 and
   // n=2 572 -> 591, but PAIR (shared-memory partner ring) 590-609 -> 561 and
-  // bf16 DBT 388 -> 377, so those keep 2)
+  // bf16 DBT 388 -> 377, so those keep 2).  At ~120 registers per thread only
+  // 2 such CTAs are resident per SM; the rest start as the first ones finish.
+  // That cannot deadlock: CTA b of a rank waits only on CTA b of other ranks
+  // (chunk c is served by CTA (c - c_lo) mod g everywhere), and every rank
+  // makes its low-index CTAs resident first.
   const int threads = cta_threads(c, 256);
   const int per_sm = !pair && dt == HFR_FLOAT32 ? 3 : 2;
   const uint64_t nch = (a.half_len[0] + C - 1) / C;  // half 0 is the longer one

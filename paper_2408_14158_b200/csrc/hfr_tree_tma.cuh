@@ -344,7 +344,6 @@ __global__ void __launch_bounds__(kTreeThreads) hfr_tree_tma_kernel(const Args a
         if (PAIR) st_relaxed_sys(&a.pad[partner]->pdown[lc], ep);
       }
     };
-    // retire jobs [retired, upto): their bulk groups are complete
     // Retire jobs [retired, upto): their bulk groups have COMPLETED (the
     // writes are performed at the destination), so the flag store that follows
     // cannot overtake them.  A system fence is needed only to order the plain
