@@ -26,7 +26,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--virtual", type=int, default=0)
     p.add_argument("--sizes", default=str(186 << 20), help="comma list of bytes per rank")
-    p.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    p.add_argument("--dtype", default="f32", choices=["f32", "bf16", "f16", "e4m3", "e5m2"])
     p.add_argument("--algos", default="flat")
     p.add_argument("--chunks", default="0")
     p.add_argument("--ctas", default="0")
@@ -61,8 +61,9 @@ def main():
     if multi:
         dist.init_process_group("nccl", device_id=dev)
     n = world if multi else a.virtual
-    tdt = torch.bfloat16 if a.dtype == "bf16" else torch.float32
-    esz = 2 if a.dtype == "bf16" else 4
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16, "f16": torch.float16, "e4m3": torch.float8_e4m3fn,
+           "e5m2": torch.float8_e5m2}[a.dtype]
+    esz = torch.tensor([], dtype=tdt).element_size()
     sizes = [int(s) for s in a.sizes.split(",")]
     comm = (hfr.Comm.init(device=local, config=hfr.Config(nvls_bytes=a.nvls, oneshot_max_bytes=a.oneshot_max))
             if multi else hfr.Comm.virtual_ranks(n, local, hfr.Config(oneshot_max_bytes=a.oneshot_max)))
@@ -70,7 +71,7 @@ def main():
     bufs = comm.empty(big, tdt)
     bufs = bufs if isinstance(bufs, list) else [bufs]
     for b in bufs:
-        b.normal_()
+        b.copy_(torch.randn(b.numel(), device=b.device).to(tdt))
     stream = torch.cuda.current_stream()
     out = open(a.out, "a") if (a.out and rank == 0) else None
 
@@ -169,14 +170,18 @@ def main():
                   "us": t * 1e6,
                   "busbw": size / t * fac / 1e9, "algbw": size / t / 1e9, **skew})
         if multi and a.nccl:
-            t_ = torch.empty(cnt, dtype=tdt, device=dev).normal_()
+            t_ = torch.randn(cnt, device=dev).to(tdt)
             o_ = torch.empty(cnt // n, dtype=tdt, device=dev)
             nfn = {"allreduce": lambda: dist.all_reduce(t_),
                    "reduce_scatter": lambda: dist.reduce_scatter_tensor(o_, t_[: o_.numel() * n]),
                    "allgather": lambda: dist.all_gather_into_tensor(t_[: o_.numel() * n], o_),
                    "reduce": lambda: dist.reduce(t_, 0),
                    "broadcast": lambda: dist.broadcast(t_, 0)}[a.coll]
-            tn = timeit(nfn, iters)
+            try:
+                tn = timeit(nfn, iters)
+            except (RuntimeError, TypeError) as e:  # e.g. NCCL without this dtype
+                emit({"impl": "nccl", "coll": a.coll, "n": n, "dtype": a.dtype, "bytes": size, "unsupported": str(e)[:200]})
+                continue
             emit({"impl": "nccl", "coll": a.coll, "n": n, "graph": a.graph, "dtype": a.dtype, "bytes": size,
                   "us": tn * 1e6, "busbw": size / tn * fac / 1e9, "algbw": size / tn / 1e9, **skew,
                   # the loaded library's version (the image's NCCL_VERSION env names the system
