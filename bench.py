@@ -340,8 +340,8 @@ def committed_traffic(key: str):
 def variant_dir_bytes(hfr, algo: str, n: int, S: int, esz: int) -> float:
     """Algorithmic NVLink bytes per direction of the busiest rank for one
     allreduce of S bytes per rank, from the trees the
-    library builds (hfr_tree_query): up-pass partials fp32 (16-bit DBT leaves
-    send raw 16-bit values), down pass in the buffer dtype; PAIR adds the pair
+    library builds (hfr_tree_query): up-pass partials fp32 (16-bit and FP8
+    DBT leaves send their raw values), down pass in the buffer dtype; PAIR adds the pair
     reduce-scatter and all-gather halves; NVLS (n+1)/n·S."""
     if algo == "nvls":
         return (n + 1) / n * S
@@ -355,7 +355,7 @@ def variant_dir_bytes(hfr, algo: str, n: int, S: int, esz: int) -> float:
         parent, children = hfr.tree_query(m, which)
         for v in range(m):
             for c in children[v]:
-                up = (esz if (not pair and esz == 2 and not children[c]) else 4) * data / 2
+                up = (esz if (not pair and esz < 4 and not children[c]) else 4) * data / 2
                 eg[c] += up
                 ing[v] += up
                 eg[v] += esz * data / 2     # final chunk down to the child

@@ -1390,29 +1390,44 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
     char* const pbuf = PAIR ? a.buf[partner] : nullptr;
     float* const dst_part = root ? nullptr : a.part[member(nd.parent)] + (uint64_t)nd.slot * a.part_stride;
     const int nchild = nd.nchild, self_pos = nd.self_pos;
-    // A DBT leaf's partial is its own x: stream it as a copy with 4 x 16 B in
-    // flight per thread (r01: DBT n=4 313 -> 360-378 GB/s).  bf16 leaves send
-    // their raw bf16 (the parent widens exactly), halving leaf traffic.
-    const bool leafcopy = !PAIR && nchild == 0 && !root && E::kPerVec <= 8;  // FP8 leaves go through unit()
-    // slot sl of this node holds a raw-bf16 leaf partial?
+    // A DBT leaf's partial is its own x: stream it as a copy with 4 vectors in
+    // flight per thread (r01: DBT n=4 313 -> 360-378 GB/s).  16-bit and FP8
+    // leaves send their raw values (the parent widens exactly): half / a
+    // quarter of an fp32 partial's bytes.
+    constexpr bool kRaw = E::kPerVec >= 8;  // 16-bit and 8-bit element types
+    const bool leafcopy = !PAIR && nchild == 0 && !root;
+    // slot sl of this node holds a raw leaf partial?
     bool slot_bf16[2] = {false, false};
-    if constexpr (!PAIR && E::kPerVec == 8) {
+    if constexpr (!PAIR && kRaw) {
       for (int sl = 0; sl < nchild; ++sl) slot_bf16[sl] = a.tree[c & 1][nd.child[sl]].nchild == 0;
     }
-    if (leafcopy && E::kPerVec == 8) {
-      // raw 16-bit partials live in the first half of the chunk's fp32 slot
-      // region (bytes [4*e0, 4*e0 + 2*C)), so they never overlap another
-      // chunk's fp32 partials in the same slot array
-      const char* srcb = mybuf + (base + e0) * 2;
+    if (leafcopy && kRaw) {
+      // raw partials live at the start of the chunk's fp32 slot region (bytes
+      // [4*e0, 4*e0 + esz*C)), so they never overlap another chunk's fp32
+      // partials in the same slot array; one 8-element unit = 16 B (16-bit) or
+      // 8 B (FP8)
+      constexpr uint64_t esz = sizeof(typename E::T);
+      const char* srcb = mybuf + (base + e0) * esz;
       char* dstb = reinterpret_cast<char*>(dst_part + e0);
       for (uint64_t q0 = threadIdx.x; q0 < nv; q0 += (uint64_t)blockDim.x * 4) {
-        uint4 v[4];
+        if constexpr (esz == 2) {
+          uint4 v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (q0 + (uint64_t)u * blockDim.x < nv) v[u] = ld128(srcb + (q0 + (uint64_t)u * blockDim.x) * 16);
+          for (int u = 0; u < 4; ++u)
+            if (q0 + (uint64_t)u * blockDim.x < nv) v[u] = ld128(srcb + (q0 + (uint64_t)u * blockDim.x) * 16);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (q0 + (uint64_t)u * blockDim.x < nv) st128(dstb + (q0 + (uint64_t)u * blockDim.x) * 16, v[u]);
+          for (int u = 0; u < 4; ++u)
+            if (q0 + (uint64_t)u * blockDim.x < nv) st128(dstb + (q0 + (uint64_t)u * blockDim.x) * 16, v[u]);
+        } else {
+          uint2 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (q0 + (uint64_t)u * blockDim.x < nv)
+              v[u] = *reinterpret_cast<const uint2*>(srcb + (q0 + (uint64_t)u * blockDim.x) * 8);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (q0 + (uint64_t)u * blockDim.x < nv) *reinterpret_cast<uint2*>(dstb + (q0 + (uint64_t)u * blockDim.x) * 8) = v[u];
+        }
       }
     } else if (leafcopy) {
       const uint64_t nq = nv * 2;  // 16 B fp32 quads
@@ -1422,7 +1437,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
         for (int u = 0; u < 4; ++u) {
           const uint64_t q = q0 + (uint64_t)u * blockDim.x;
           if (q < nq) {
-            F32::widen(ld128(mybuf + (base + e0 + q * 4) * 4), f[u]);  // fp32 only (16-bit: raw copy above)
+            F32::widen(ld128(mybuf + (base + e0 + q * 4) * 4), f[u]);  // fp32 only (16/8-bit: raw copy above)
           }
         }
 #pragma unroll
@@ -1446,7 +1461,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
 #pragma unroll
       for (int sl = 0; sl < 2; ++sl)
         if (sl < nchild) {
-          if (E::kPerVec == 8 && slot_bf16[sl])
+          if (kRaw && slot_bf16[sl])
             load8<E>(reinterpret_cast<const char*>(mypart + (uint64_t)sl * a.part_stride + e0), e - e0, pp[sl]);
           else
             load8_f32(mypart + (uint64_t)sl * a.part_stride, e, pp[sl]);
@@ -1514,7 +1529,7 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
         if (k != nd.self_pos) {
           const int sl = k < nd.self_pos ? k : k - 1;
           const float* slot = mypart + (uint64_t)sl * a.part_stride;
-          s = (E::kPerVec == 8 && slot_bf16[sl]) ? E::load1(reinterpret_cast<const char*>(slot + e0), e - e0) : slot[e];
+          s = (kRaw && slot_bf16[sl]) ? E::load1(reinterpret_cast<const char*>(slot + e0), e - e0) : slot[e];
         }
         acc = k == 0 ? s : __fadd_rn(acc, s);
       }
@@ -1523,8 +1538,8 @@ __global__ void __launch_bounds__(512) hfr_tree_kernel(const Args a) {
         E::store1(mybuf, base + e, acc);
         for (int k = 0; k < nd.nchild; ++k) E::store1(a.buf[member(nd.child[k])], base + e, acc);
         if constexpr (PAIR) E::store1(pbuf, base + e, acc);
-      } else if (E::kPerVec == 8 && leafcopy) {
-        E::store1(reinterpret_cast<char*>(dst_part + e0), e - e0, acc);  // raw 16-bit leaf partial (exact)
+      } else if (kRaw && leafcopy) {
+        E::store1(reinterpret_cast<char*>(dst_part + e0), e - e0, acc);  // raw 16/8-bit leaf partial (exact)
       } else {
         dst_part[e] = acc;
       }

@@ -78,3 +78,12 @@ def test_variant_bytes_bf16_dbt_between_2_and_3():
     S = 1 << 20
     v = bench.variant_dir_bytes(hfr, "dbt", 8, S, 2) / S
     assert 2.0 <= v <= 3.0
+
+
+def test_variant_bytes_fp8_dbt_leaves_raw():
+    """FP8 DBT leaves send 1-byte raw values, not 4-byte fp32 partials."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2408_14158_b200 as hfr
+    S = 1 << 20
+    assert bench.variant_dir_bytes(hfr, "dbt", 2, S, 1) == pytest.approx(S * (1 + 1) / 2)  # n=2: raw up + final down
