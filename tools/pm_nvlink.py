@@ -26,7 +26,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 SRC = os.path.join(ROOT, "tools", "pm_sampler.cu")
 LIB = os.path.join(ROOT, "tools", "libpm_sampler.so")
-WANT = [r"^nvltx__bytes$", r"^nvlrx__bytes$", r"^dram__bytes_read$", r"^dram__bytes_write$"]
+WANT = [r"^nvltx__bytes$", r"^nvlrx__bytes$", r"^nvltx__bytes_data_user$", r"^nvlrx__bytes_data_user$",
+        r"^dram__bytes_read$", r"^dram__bytes_write$"]
 
 
 def lib():
@@ -46,6 +47,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--interval", type=int, default=20000, help="sampling interval (GPU sysclk cycles)")
     ap.add_argument("--out", default="")
+    ap.add_argument("--algo", default="flat")
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -66,9 +69,12 @@ def main():
     base = buf.value.decode().split()
     picked = [m for m in base if any(re.match(w, m) for w in WANT)]
     metrics = [m + ".sum" for m in picked]
-    comm = hfr.Comm.init(device=local, config=hfr.Config(algo="flat", scale=1.0 / world, timeout_ms=60000))
-    count = (186 << 20) // 4
-    t = comm.empty(count, torch.float32)
+    nvls = (200 << 20) if a.algo == "nvls" else 0
+    comm = hfr.Comm.init(device=local, config=hfr.Config(algo=a.algo, scale=1.0 / world, timeout_ms=60000,
+                                                         nvls_bytes=nvls))
+    esz = 2 if a.dtype == "bf16" else 4
+    count = (186 << 20) // esz
+    t = comm.empty(count, torch.bfloat16 if a.dtype == "bf16" else torch.float32)
     t.normal_()
     for _ in range(3):
         comm.allreduce(t)
@@ -76,8 +82,9 @@ def main():
     dist.barrier()
     comm.barrier()
     torch.cuda.synchronize()
-    res = {"rank": rank, "n": world, "steps": a.steps, "query_count": nq, "metrics": metrics,
-           "nvl_base_metrics": [m for m in base if "nvl" in m][:40]}
+    import bench
+    res = {"rank": rank, "n": world, "algo": a.algo, "dtype": a.dtype, "count": count, "steps": a.steps,
+           "query_count": nq, "metrics": metrics, "source_sha": bench.source_sha()}
     if metrics:
         rc = L.pm_start(local, ",".join(metrics).encode(), a.interval, 1 << 16)
         res["start_rc"] = rc
@@ -94,9 +101,9 @@ def main():
             res.update({"samples": ns, "window_ns": t1.value - t0.value, "timed_ms": e0.elapsed_time(e1),
                         "sum": dict(zip(metrics, list(sums))),
                         "per_launch": {m: v / a.steps for m, v in zip(metrics, list(sums))}})
-    S = count * 4
-    res["algorithmic_per_launch"] = {"nvlink_bytes_per_direction": 2.0 * (world - 1) / world * S,
-                                     "dram_bytes": 2.0 * S}
+    S = count * esz
+    res["algorithmic_per_launch"] = {"nvlink_bytes_per_direction": bench.variant_dir_bytes(hfr, a.algo, world, S, esz)
+                                     if a.algo != "flat" else 2.0 * (world - 1) / world * S, "dram_bytes": 2.0 * S}
     res["status"] = hfr.status_string(comm.status())
     allr = [None] * world
     dist.all_gather_object(allr, res)

@@ -54,8 +54,33 @@ def metrics_from_rep(path: str) -> dict:
     return out
 
 
+def record_from_pm(path: str, kernel: str = "hfr_flat_tma_kernel"):
+    """profiles/traffic.json entries from a tools/pm_nvlink.py result (CUPTI
+    PM sampling over K launches at N>1): rank 0's bytes per launch, keyed like
+    bench.py's N>1 roofline (`<kernel>:<algo>:<n>:<dtype>:<count>:nvlink`)."""
+    d = json.loads(open(path).read().strip().splitlines()[-1])
+    r0 = d["ranks"][0]
+    pl = r0["per_launch"]
+    key = f"{kernel}:{r0['algo']}:{r0['n']}:{r0['dtype']}:{r0['count']}:nvlink"
+    rec = {"source": os.path.relpath(path, ROOT) + " (CUPTI PM sampling, tools/pm_nvlink.py, rank 0, "
+                      f"{r0['steps']} launches)", "source_sha": r0["source_sha"],
+           "nvltx_bytes": pl.get("nvltx__bytes.sum"), "nvlrx_bytes": pl.get("nvlrx__bytes.sum"),
+           "nvltx_user_bytes": pl.get("nvltx__bytes_data_user.sum"),
+           "nvlrx_user_bytes": pl.get("nvlrx__bytes_data_user.sum"),
+           "dram_bytes": (pl.get("dram__bytes_read.sum") or 0) + (pl.get("dram__bytes_write.sum") or 0)}
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
+    traffic[key] = rec
+    json.dump(traffic, open(tpath, "w"), indent=1, sort_keys=True)
+    print(key, json.dumps(rec))
+
+
 def main():
     args = sys.argv[1:]
+    if args and args[0] == "--from-pm":
+        for p in args[1:]:
+            record_from_pm(p)
+        return
     note = None
     if "--note" in args:
         i = args.index("--note")
