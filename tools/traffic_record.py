@@ -54,14 +54,18 @@ def metrics_from_rep(path: str) -> dict:
     return out
 
 
-def record_from_pm(path: str, kernel: str = "hfr_flat_tma_kernel"):
+KERNEL_OF = {"flat": "hfr_flat_tma_kernel", "dbt": "hfr_tree_kernel", "pair_dbt": "hfr_tree_kernel",
+             "nvls": "hfr_nvls_kernel"}
+
+
+def record_from_pm(path: str):
     """profiles/traffic.json entries from a tools/pm_nvlink.py result (CUPTI
     PM sampling over K launches at N>1): rank 0's bytes per launch, keyed like
     bench.py's N>1 roofline (`<kernel>:<algo>:<n>:<dtype>:<count>:nvlink`)."""
     d = json.loads(open(path).read().strip().splitlines()[-1])
     r0 = d["ranks"][0]
     pl = r0["per_launch"]
-    key = f"{kernel}:{r0['algo']}:{r0['n']}:{r0['dtype']}:{r0['count']}:nvlink"
+    key = f"{KERNEL_OF.get(r0['algo'], r0['algo'])}:{r0['algo']}:{r0['n']}:{r0['dtype']}:{r0['count']}:nvlink"
     rec = {"source": os.path.relpath(path, ROOT) + " (CUPTI PM sampling, tools/pm_nvlink.py, rank 0, "
                       f"{r0['steps']} launches)", "source_sha": r0["source_sha"],
            "nvltx_bytes": pl.get("nvltx__bytes.sum"), "nvlrx_bytes": pl.get("nvlrx__bytes.sum"),
