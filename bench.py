@@ -503,8 +503,15 @@ def main():
                 "frac": achieved / peak, "frac_of_nominal": achieved / NVLINK_NOMINAL_GBS,
                 "frac_of_guide": achieved / NVLINK_GUIDE_GBS,  # B200_PROFILING.md's measured peer copy
                 "nominal": NVLINK_NOMINAL_GBS,
-                "traffic": (max(trec.get("nvltx_bytes", 0), trec.get("nvlrx_bytes", 0)) or None) if trec else None,
-                "traffic_kind": "ncu nvltx/nvlrx bytes per launch, the larger direction (rank 0)",
+                # CUPTI PM-sampled NVLink bytes per launch (tools/pm_nvlink.py), the larger
+                # direction of rank 0: the user payload (comparable with the algorithmic
+                # bytes) and what crossed the wire incl. packet protocol
+                "traffic": (max(trec.get("nvltx_user_bytes") or 0, trec.get("nvlrx_user_bytes") or 0)
+                            or None) if trec else None,
+                "traffic_kind": "NVLink user-payload bytes per launch (CUPTI PM sampling, nvltx/nvlrx "
+                                "__bytes_data_user, larger direction, rank 0)",
+                "traffic_wire": (max(trec.get("nvltx_bytes") or 0, trec.get("nvlrx_bytes") or 0) or None)
+                if trec else None,
                 "dram_traffic": trec.get("dram_bytes") if trec else None,
                 "traffic_provenance": tprov,
                 "kernel": kname, "algorithmic_bytes_per_launch": nv_bytes,
