@@ -62,6 +62,9 @@ def main():
     ap.add_argument("--tail", type=int, default=1, help="1: buckets completed by the last gradient GEMM (embed) "
                                                        "use a full-width config (nothing left to overlap)")
     ap.add_argument("--tail-algo", default="flat")
+    ap.add_argument("--clock-phases", type=int, default=0,
+                    help="N > 0: afterwards, N backwards alone then N with the allreduces, each block under its own "
+                         "clock sampler (does the comm lower the power-capped SM clock?)")
     a = ap.parse_args()
 
     import torch
@@ -157,6 +160,12 @@ def main():
                          ("comm_full", comm_full)):
             res[name].append(timed(fn))
     clk = {"all": ck.stop()}
+    if a.clock_phases:
+        for name, fn in (("bwd_only", lambda: backward(False)), ("bwd_with_comm", lambda: backward(True))):
+            c = Clocks(local, interval_ms=20)
+            c.start()
+            ts = [timed(fn) for _ in range(a.clock_phases)]
+            clk[name] = dict(c.stop(), median_ms=statistics.median(ts) * 1e3)
     if comm.status() != hfr.SUCCESS:
         raise SystemExit(hfr.status_string(comm.status()))
     tb, tc, tt, tf = (statistics.median(res[k]) for k in ("bwd", "comm", "both", "comm_full"))
