@@ -443,3 +443,26 @@ def test_flat_staging_modes(hfr, staging, n, dtype, N):
     xs = gen.rank_inputs(n, N, dtype, "normal", seed_base=4400 + N)
     outs = run_cfg(hfr, n, xs, hfr.Config(algo="flat", scale=0.5, flat_staging=staging))
     check(outs, O.fold_ascending(xs, 0.5), f"flat staging={staging} n={n} {dtype} N={N}")
+
+
+@pytest.mark.parametrize("n", [11, 16])
+@pytest.mark.parametrize("algo", ["flat", "oneshot", "dbt", "pair_dbt", "ce", "auto"])
+@pytest.mark.parametrize("dtype", [gen.FP32, gen.BF16, gen.E4M3])
+def test_parity_beyond_one_box(hfr, n, algo, dtype):
+    """More ranks than one 8-GPU box (the library allows up to 16): the
+    generic-n kernels (no compile-time rank count), deeper double binary
+    trees (odd n: rank 0 interior in both trees, reading R9) — bit-exact."""
+    if algo == "pair_dbt" and n % 2:
+        pytest.skip("pair-first needs even n")
+    N = 100_003
+    xs = gen.rank_inputs(n, N, dtype, "normal", seed_base=5100 + n)
+    comm = comm_for(hfr, n)
+    comm.set_config(hfr.Config(algo=algo, chunk_elems=1024, scale=1.0 / n, timeout_ms=20000))
+    bufs = comm.empty(N, torch_dtype(dtype))
+    for b, x in zip(bufs, xs):
+        b.copy_(to_torch(x, "cuda:0"))
+    comm.allreduce_virtual(bufs)
+    torch.cuda.synchronize()
+    assert comm.status() == hfr.SUCCESS, hfr.status_string(comm.status())
+    want = O.allreduce(xs, algo, chunk_elems=1024, scale=1.0 / n)[0]
+    check([to_numpy(b) for b in bufs], want, f"{algo} n={n} {dtype}")
