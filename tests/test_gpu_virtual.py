@@ -87,7 +87,7 @@ def test_parity_distributions(hfr, dist, dtype, algo):
 
 
 @pytest.mark.parametrize("algo", ALGOS)
-@pytest.mark.parametrize("scale", [0.1, 3.0])
+@pytest.mark.parametrize("scale", [0.1, 3.0, -0.5, 0.0, float("inf")])
 def test_parity_scale(hfr, algo, scale):
     xs = gen.rank_inputs(4, 20_000, gen.FP32, "normal", seed_base=5)
     outs = run(hfr, 4, xs, algo, chunk=1024, scale=scale)
