@@ -37,6 +37,7 @@ def lib():
     L = ctypes.CDLL(LIB)
     L.pm_query_metrics.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t]
     L.pm_start.argtypes = [ctypes.c_int, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_uint64]
+    L.pm_series.argtypes = [ctypes.c_char_p]
     L.pm_stop.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int, ctypes.POINTER(ctypes.c_uint64),
                           ctypes.POINTER(ctypes.c_uint64)]
     return L
@@ -49,6 +50,7 @@ def main():
     ap.add_argument("--out", default="")
     ap.add_argument("--algo", default="flat")
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--series", default="", help="per-sample CSV prefix (rank r writes <prefix>_rank<r>.csv)")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -86,6 +88,8 @@ def main():
     res = {"rank": rank, "n": world, "algo": a.algo, "dtype": a.dtype, "count": count, "steps": a.steps,
            "query_count": nq, "metrics": metrics, "source_sha": bench.source_sha()}
     if metrics:
+        if a.series:
+            L.pm_series(f"{a.series}_rank{rank}.csv".encode())
         rc = L.pm_start(local, ",".join(metrics).encode(), a.interval, 1 << 16)
         res["start_rc"] = rc
         if rc == 0:

@@ -55,6 +55,7 @@ struct Session {
   std::atomic<bool> stop{false};
   std::mutex mu;
   int error = 0;
+  FILE* series = nullptr;  // optional per-sample dump: start_ns,end_ns,metric values...
 } g;
 
 int host_init(int dev, CUpti_ProfilerType type) {
@@ -110,6 +111,11 @@ int drain() {
     PM_TRY(cuptiProfilerHostEvaluateToGpuValues(&ev));
     std::lock_guard<std::mutex> lock(g.mu);
     for (size_t i = 0; i < v.size(); ++i) g.sums[i] += v[i];
+    if (g.series) {
+      fprintf(g.series, "%llu,%llu", (unsigned long long)si.startTimestamp, (unsigned long long)si.endTimestamp);
+      for (double x : v) fprintf(g.series, ",%.0f", x);
+      fprintf(g.series, "\n");
+    }
     if (!g.samples) g.t_first = si.startTimestamp;
     g.t_last = si.endTimestamp;
     ++g.samples;
@@ -140,6 +146,12 @@ extern "C" int pm_query_metrics(int dev, char* buf, size_t size) {
   cuptiProfilerHostDeinitialize(&dp);
   g.host = nullptr;
   return (int)bp.numMetrics;
+}
+
+extern "C" int pm_series(const char* path) {  // call before pm_start; NULL / "" = off
+  if (g.series) fclose(g.series);
+  g.series = (path && *path) ? fopen(path, "w") : nullptr;
+  return g.series || !(path && *path) ? 0 : -1;
 }
 
 extern "C" int pm_start(int dev, const char* metrics_csv, uint64_t interval, uint64_t max_samples) {
@@ -234,5 +246,9 @@ extern "C" int pm_stop(double* sums, int n, uint64_t* t_first, uint64_t* t_last)
   cuptiProfilerDeInitialize(&pd);
   g.host = nullptr;
   g.sampler = nullptr;
+  if (g.series) {
+    fclose(g.series);
+    g.series = nullptr;
+  }
   return (int)g.samples;
 }
